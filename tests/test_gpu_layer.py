@@ -1,0 +1,179 @@
+"""GPU parity of SpikingLayer (CUDA path through the C ABI) against the
+reference: golden fixtures produced by the reference itself, plus the oracle
+at the benchmark's full sizes on channel subsets (channels are independent in
+forward and backward, so a subset is an exact restatement of the full job)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import psn_oracle as O
+from tests.parity import assert_close_scaled, assert_rel, spikes_match_except_ties
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+MANIFEST = json.load(open(os.path.join(GOLDEN, "manifest.json")))
+CASES = {c["name"]: c for c in MANIFEST["layer_cases"]}
+
+
+def _P():
+    import paper_2501_14490_b200 as P
+    return P
+
+
+def _layer_from_fixture(meta, z):
+    P = _P()
+    f = meta["flags"]
+    kind, alpha = f.get("surrogate", ["arctan", 2.0])
+    cfg = P.NeuronConfig(channels=meta["shape"][2], order=meta["k"], dilation=meta["d"],
+                         weight_sharing=P.WeightSharing.SHARED if f.get("shared") else P.WeightSharing.CHANNEL_WISE,
+                         quantized=f.get("quantized", True),
+                         grad_mode=P.QuantGradMode.ROUND_STE if f.get("grad_mode") == "round_ste"
+                         else P.QuantGradMode.WHOLE_STE)
+    layer = P.SpikingLayer(cfg, surrogate=P.SurrogateConfig(P.SurrogateKind(kind), alpha),
+                           fuse_from_batch_stats=f.get("fuse_from_batch_stats", True), device="cuda")
+    layer.quantize_in_smooth_mode = bool(f.get("quantize_in_smooth_mode", False))
+    with torch.no_grad():
+        layer.W.copy_(torch.from_numpy(z["W"]))
+        layer.gamma.copy_(torch.from_numpy(z["gamma"]))
+        layer.beta.copy_(torch.from_numpy(z["beta"]))
+        layer.running_mean.copy_(torch.from_numpy(z["running_mean_in"]))
+        layer.running_var.copy_(torch.from_numpy(z["running_var_in"]))
+    return layer
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_layer_matches_reference_fixture(name):
+    P = _P()
+    meta = CASES[name]
+    z = np.load(os.path.join(GOLDEN, f"layer_{name}.npz"))
+    layer = _layer_from_fixture(meta, z)
+    smooth = meta["mode"] == "smooth"
+    mode = P.Mode.SMOOTH if smooth else P.Mode.TRAIN
+    f64 = meta["dtype"] == "float64"
+    gtol = 1e-9 if f64 else 1e-5
+    d = meta["d"]
+    for step in range(2):
+        pre = f"s{step}_"
+        x = torch.tensor(z[pre + "x"], device="cuda", requires_grad=True)
+        out = layer(x, mode)
+        st = {k: v.cpu().numpy() for k, v in layer.last_state().items()}
+        assert_rel(st["mu"], z[pre + "mu"], 1e-11, "mu")
+        assert_rel(st["s"], z[pre + "s"], 1e-12, "s")
+        assert_rel(st["a"], z[pre + "a"], 1e-12, "a")
+        assert_close_scaled(st["b_f"], z[pre + "b_f"], 1e-12, "b_f")
+        assert_rel(st["w_f"], z[pre + "w_f"], 1e-12, "w_f")
+        if meta["flags"].get("quantized", True) and (not smooth or meta["flags"].get("quantize_in_smooth_mode")):
+            assert np.array_equal(st["w_q"], z[pre + "w_q"]), "quantized weights differ"
+        else:
+            assert_rel(st["w_q"], z[pre + "w_q"], 1e-12, "w_q (float)")
+        assert_rel(layer.running_mean.cpu().numpy(), z[pre + "running_mean"], 1e-10, "running_mean")
+        assert_rel(layer.running_var.cpu().numpy(), z[pre + "running_var"], 1e-12, "running_var")
+        got = out.detach().cpu().numpy()
+        assert got.dtype == z[pre + "x"].dtype
+        if smooth:
+            assert_close_scaled(got, z[pre + "out"], 1e-12 if f64 else 1e-6, "smooth output")
+        else:
+            spikes_match_except_ties(got, z[pre + "out"], z[pre + "x"], z[pre + "w_q"], z[pre + "b_f"], d)
+        layer.zero_grad(set_to_none=True)
+        out.backward(torch.tensor(z[pre + "dy"], device="cuda"))
+        assert_close_scaled(x.grad.cpu().numpy(), z[pre + "dx"], gtol, "dx")
+        assert_close_scaled(layer.W.grad.cpu().numpy(), z[pre + "dW"], gtol, "dW")
+        assert_close_scaled(layer.gamma.grad.cpu().numpy(), z[pre + "dgamma"], gtol, "dgamma")
+        assert_close_scaled(layer.beta.grad.cpu().numpy(), z[pre + "dbeta"], gtol, "dbeta")
+    # EVAL with the running statistics after the two steps (network.py:219-234)
+    layer.eval()
+    xe = torch.tensor(z["eval_x"], device="cuda")
+    got = layer(xe).cpu().numpy()
+    p = O.LayerParams(W=z["W"], gamma=z["gamma"], beta=z["beta"],
+                      running_mean=layer.running_mean.cpu().numpy(),
+                      running_var=layer.running_var.cpu().numpy(), d=d,
+                      quantized=meta["flags"].get("quantized", True))
+    w_f, b_f = O.fused_running(p)
+    w = O.dequantize(*O.quantize_pow2(w_f)) if p.quantized else w_f.astype(np.float32).astype(np.float64)
+    b = b_f.astype(np.float32).astype(np.float64)
+    spikes_match_except_ties(got, z["eval_out"], z["eval_x"].astype(np.float32), w, b, d, "eval spikes")
+
+
+def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0):
+    """Full-size GPU fwd+bwd; oracle on a channel subset (exact restatement)."""
+    P = _P()
+    rng = np.random.default_rng(seed)
+    x_np = rng.standard_normal((T, N, C)).astype(np.float32)
+    dy_np = rng.standard_normal((T, N, C)).astype(np.float32)
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(seed + 1), device="cuda")
+    x = torch.tensor(x_np, device="cuda", dtype=dtype, requires_grad=True)
+    out = layer(x, P.Mode.TRAIN)
+    out.backward(torch.tensor(dy_np, device="cuda", dtype=dtype))
+    torch.cuda.synchronize()
+    sel = np.array(channels)
+    xs = x.detach().float().cpu().numpy()[:, :, sel]
+    dys = torch.tensor(dy_np, dtype=dtype).float().numpy()[:, :, sel]
+    p = O.init_layer(len(sel), k, d, weight_init="uniform", rng=np.random.default_rng(seed + 1))
+    p.W = layer.W.detach().cpu().numpy()[sel]
+    ref_out, cache, dx, dW, dg, db = O.train_step(p, xs, dys)
+    st = {kk: v.cpu().numpy()[sel] for kk, v in layer.last_state().items()}
+    assert_rel(st["mu"], cache.mu, 1e-10, "mu")
+    assert_rel(st["a"], cache.a, 1e-12, "a")
+    assert np.array_equal(st["w_q"], cache.w_q)
+    got = out.detach().float().cpu().numpy()[:, :, sel]
+    flips = spikes_match_except_ties(got, ref_out, xs, cache.w_q, cache.b_f, d)
+    gt = 1e-5 if dtype == torch.float32 else 1e-2
+    assert_close_scaled(x.grad.float().cpu().numpy()[:, :, sel], dx, gt, "dx")
+    assert_close_scaled(layer.W.grad.cpu().numpy()[sel], dW, 1e-5, "dW")
+    assert_close_scaled(layer.gamma.grad.cpu().numpy()[sel], dg, 1e-5, "dgamma")
+    assert_close_scaled(layer.beta.grad.cpu().numpy()[sel], db, 1e-5, "dbeta")
+    return flips
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_metric_config_parity_on_channel_subset(d):
+    """T=1024, B=64, C=512, k=4 (BASELINE metric config), sawtooth d."""
+    flips = _oracle_subset_check(1024, 64, 512, 4, d, channels=[0, 1, 77, 255, 256, 400, 510, 511], seed=d)
+    assert flips <= 2
+
+
+def test_config1_full_parity():
+    """T=250, B=32, C=128, k=4 (BASELINE config 1), every channel."""
+    _oracle_subset_check(250, 32, 128, 4, 3, channels=list(range(128)), seed=11)
+
+
+@pytest.mark.parametrize("k,d", [(8, 2), (16, 3), (16, 1)])
+def test_high_order_parity(k, d):
+    _oracle_subset_check(512, 16, 96, k, d, channels=[0, 31, 32, 63, 95], seed=k + d)
+
+
+def test_bf16_io_parity():
+    """bf16 I/O: oracle runs on the bf16 inputs widened to f32."""
+    _oracle_subset_check(256, 16, 128, 2, 1, channels=[0, 5, 64, 127], dtype=torch.bfloat16, seed=5)
+
+
+def test_grads_accumulate_like_reference():
+    """Two backward passes accumulate into .grad (reference uses +=)."""
+    P = _P()
+    cfg = P.NeuronConfig(channels=16, order=3, dilation=2, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(3), device="cuda")
+    x = torch.randn(40, 4, 16, device="cuda")
+    dy = torch.randn(40, 4, 16, device="cuda")
+    layer(x, P.Mode.TRAIN).backward(dy)
+    g1 = layer.W.grad.clone()
+    layer(x, P.Mode.TRAIN).backward(dy)
+    # second forward used updated running stats only for the running update;
+    # batch-stat fusion makes both backward passes identical
+    torch.testing.assert_close(layer.W.grad, 2 * g1, rtol=1e-12, atol=0)
+
+
+def test_input_validation_errors():
+    P = _P()
+    layer = P.SpikingLayer(P.NeuronConfig(channels=4, order=2), device="cuda")
+    with pytest.raises(ValueError):
+        layer(torch.randn(5, 2, 3, device="cuda"), P.Mode.TRAIN)  # channel mismatch
+    with pytest.raises(ValueError):
+        layer(torch.randn(5, 4, device="cuda"), P.Mode.TRAIN)  # rank 2
+    with pytest.raises(ValueError):
+        layer(torch.randn(5, 2, 4), P.Mode.TRAIN)  # CPU tensor: no CPU fallback
