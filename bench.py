@@ -195,6 +195,8 @@ def main():
     sp = stream.cuda_stream
     W, gam, bet, rm, rv = layer.W.detach(), layer.gamma.detach(), layer.beta.detach(), layer.running_mean, layer.running_var
 
+    plan_f, plan_b = L.plan_info(desc, False), L.plan_info(desc, True)
+
     def fwd():
         L.check(lib.psn_forward_train(ctypes.byref(desc), x.data_ptr(), W.data_ptr(), gam.data_ptr(),
                                       bet.data_ptr(), rm.data_ptr(), rv.data_ptr(), out.data_ptr(),
@@ -244,7 +246,9 @@ def main():
     hbm, peak_src = _peaks()
     f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
     fwd_bytes, bwd_bytes = 2 * esize * nel, 3 * esize * nel
-    groups = {"forward (psn_forward_train)": (fwd_bytes, f_ms), "backward (psn_backward)": (bwd_bytes, b_ms)}
+    fname = "fused_fwd_kernel" if plan_f.get("fused") else "psn_forward_train (3 kernels)"
+    bname = "fused_bwd_kernel" if plan_b.get("fused") else "psn_backward (3 kernels)"
+    groups = {fname: (fwd_bytes, f_ms), bname: (bwd_bytes, b_ms)}
     dom_name, (dom_bytes, dom_ms) = max(groups.items(), key=lambda kv: kv[1][1])
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_achieved = (5 * esize * nel) / ((f_ms + b_ms) * 1e-3) / 1e9
@@ -316,7 +320,8 @@ def main():
                               "bytes_per_step": 5 * esize * nel, "fwd_ms": f_ms, "bwd_ms": b_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * 6,
+            "gpu_launches": K * (plan_f["launches"] + plan_b["launches"]),
+            "plan": {"forward": plan_f, "backward": plan_b},
             "clocks": clk.summary(),
             "wall_s_timed": wall,
         }

@@ -125,6 +125,13 @@ PSN_API int psn_forward_eval(const psn_desc_t *desc, const void *x, const double
                      const double *running_mean, const double *running_var,
                      void *out, void *workspace, psn_stream_t stream);
 
+/* Execution plan of psn_forward_train (backward = 0) / psn_backward (1):
+ * info[0] = 1 if the persistent fused kernel runs (else the generic 3-kernel path),
+ * info[1] = CTAs, info[2] = channel groups, info[3] = 32-column tiles per group,
+ * info[4] = row slices, info[5] = kernel launches per call (memsets included).
+ * Returns the number of entries written (<= n).                                  */
+PSN_API int psn_plan_info(const psn_desc_t *desc, int backward, int64_t *info, int n);
+
 /* ---- engine-level operators (the reference's plugin functions) ---------- */
 /* w: [w_rows, k] f64 with w_rows in {1, C}; bias: [C] f64 or NULL.
  * Carrier dtype F32 or F64; accumulation f64 in reference tap order.         */

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libpsn_b200.so")
-SOURCES = ["psn_layer.cu", "psn_engines.cu"]
+SOURCES = ["psn_layer.cu", "psn_engines.cu", "psn_fused.cu"]
 HEADERS = ["psn_common.cuh"]
 
 NVCC_FLAGS = [

@@ -32,7 +32,7 @@ EXPORTED = (
     "psn_workspace_bytes", "psn_forward_train", "psn_backward", "psn_forward_eval",
     "psn_conv_forward", "psn_conv_forward_shift", "psn_conv_forward_shift_int",
     "psn_conv_backward_input", "psn_conv_backward_weight", "psn_conv_backward_bias",
-    "psn_quantize_pow2",
+    "psn_quantize_pow2", "psn_plan_info",
 )
 
 
@@ -63,6 +63,7 @@ _SIGS = {
     "psn_conv_backward_weight": (ctypes.c_int, [_D, _P, _P, ctypes.c_int, _P, _P, _P]),
     "psn_conv_backward_bias": (ctypes.c_int, [_D, _P, _P, _P, _P]),
     "psn_quantize_pow2": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P, _P]),
+    "psn_plan_info": (ctypes.c_int, [_D, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
 }
 
 _lib = None
@@ -139,6 +140,13 @@ def stream_of(t: torch.Tensor) -> int:
 def workspace(desc: PsnDesc, device) -> torch.Tensor:
     n = lib().psn_workspace_bytes(ctypes.byref(desc))
     return torch.empty(max(int(n), 256), dtype=torch.uint8, device=device)
+
+
+def plan_info(desc: PsnDesc, backward: bool) -> dict:
+    buf = (ctypes.c_int64 * 6)()
+    n = lib().psn_plan_info(ctypes.byref(desc), int(backward), buf, 6)
+    keys = ("fused", "ctas", "groups", "tiles_per_group", "row_slices", "launches")
+    return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
 
 
 def require_cuda(*tensors) -> None:

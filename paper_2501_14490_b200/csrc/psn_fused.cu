@@ -1,0 +1,960 @@
+// psn_fused.cu — persistent, pipelined sm_100a kernels for the PSN TRAIN
+// forward and backward (reference network.py:236-318).
+//
+// Why persistent: the BN batch statistics put a global reduction between the
+// two passes of each direction (forward: stats of h1 -> spikes from h2;
+// backward: per-channel sums -> dx).  A naive 2-pass design streams x twice
+// (and dy twice) from HBM: 32 B/elem against the 20 B/elem algorithmic
+// minimum.  Here the channels are cut into groups whose data fits comfortably
+// in the 126 MB L2; every warp of the (co-resident, cooperative) grid works on
+// every group, and the passes are software-pipelined across groups:
+//
+//     iteration it:  pass1(it)  |  fold(it-1)  |  pass2(it-LAG)
+//
+// pass1 streams group `it` from HBM (L2 evict_last) and publishes per-CTA
+// partial sums; the fold of group it-1 (one warp per channel, deterministic
+// fixed-order sums) runs once every CTA has arrived; pass2 re-reads group
+// it-LAG from L2 (evict_first) while the barrier/fold latency of later groups
+// hides behind pass1 of the next group.  HBM traffic ~= 20 B/elem.
+//
+// Exactness (forward): h1 = sum_i W_i x_i accumulated in f64 (DFMA, reference
+// tap order) and rounded to f32 with a 2-DADD magic-number rounding (the
+// F2F.F32.F64 instruction runs at ~8/clk/SM on B200); h2 = sum_i w_q,i x_i +
+// b_f in f64 with exact power-of-two products (DFMA == mul-then-add there), so
+// spikes equal the reference's whenever (w_q, b_f) do; the Heaviside compares
+// h2 against -2^-150, which is exactly "f32(h2) >= 0".  Backward arithmetic is
+// f32 (FFMA) with f64 accumulation of the per-channel sums every U steps.
+#include <string.h>
+
+#include <mutex>
+#include <type_traits>
+
+#include "psn_common.cuh"
+
+namespace psn {
+
+// ---------------------------------------------------------------------------
+// PTX helpers: L2 cache policies, coherent loads, release/acquire counters
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float ldh(const float* a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldh(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return (float)v;
+}
+__device__ __forceinline__ float ldh(const __nv_bfloat16* a, uint64_t pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
+  return __uint_as_float(((unsigned)v) << 16);
+}
+// exact widening loads for the f64 forward (double carrier keeps all bits)
+__device__ __forceinline__ double ldhw(const float* a, uint64_t pol) { return (double)ldh(a, pol); }
+__device__ __forceinline__ double ldhw(const __nv_bfloat16* a, uint64_t pol) { return (double)ldh(a, pol); }
+__device__ __forceinline__ double ldhw(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void sth(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void sth(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void sth(__nv_bfloat16* a, double v, uint64_t pol) {
+  const __nv_bfloat16 b = __float2bfloat16_rn((float)v);
+  const unsigned short u = *reinterpret_cast<const unsigned short*>(&b);
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(a), "h"(u), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void sth(float* a, double v, uint64_t pol) { sth(a, (float)v, pol); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release(unsigned* a, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_geq(const unsigned* a, unsigned target) {
+  while (ld_acquire(a) < target) __nanosleep(64);
+}
+
+// f32 rounding of an f64 value with two DADDs (exact (double)(float)h for every
+// |h| below FLT_MAX, denormals included): adding M = 1.5 * 2^(E+29) moves the
+// rounding point of the sum to 2^(E-23) = ulp_f32(h), ties-to-even preserved.
+__device__ __forceinline__ double round_f32(double h) {
+  unsigned ex = (unsigned)__double2hiint(h) & 0x7ff00000u;
+  ex = ex < 0x38100000u ? 0x38100000u : ex;  // f32 denormal range: ulp fixed at 2^-149
+  const double M = __hiloint2double((int)(ex + (29u << 20) + 0x00080000u), 0);
+  return __dsub_rn(__dadd_rn(h, M), M);
+}
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+// FPlan is declared in psn_common.cuh
+
+
+// row index -> (n, r, s, S_r)
+__device__ __forceinline__ void row_decode(const FPlan& P, int64_t rho, int64_t& n, int& r, int64_t& s,
+                                           int64_t& Sr) {
+  n = rho / P.T;
+  const int64_t rem = rho - n * P.T;
+  const int64_t big = (int64_t)P.m * (P.q + 1);
+  if (rem < big) {
+    r = (int)(rem / (P.q + 1));
+    s = rem - (int64_t)r * (P.q + 1);
+    Sr = P.q + 1;
+  } else {
+    const int64_t t2 = rem - big;
+    const int64_t rr = t2 / P.q;
+    r = P.m + (int)rr;
+    s = t2 - rr * P.q;
+    Sr = P.q;
+  }
+}
+
+constexpr int kLag = 2;  // pass2 runs kLag iterations behind pass1
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <int K, typename IO, int U>
+__device__ __forceinline__ void fwd_pass1_piece(const IO* __restrict__ base, int64_t step, int64_t s0, int64_t len,
+                                                bool cv, const double (&w)[K], double sh, double& S1, double& S2,
+                                                uint64_t pol) {
+  double xw[K];
+#pragma unroll
+  for (int m = 1; m < K; ++m) {
+    const int64_t sp = s0 - K + m;
+    xw[m] = (cv && sp >= 0) ? ldhw(base + (int64_t)(m - K) * step, pol) : 0.0;
+  }
+  for (int64_t s = 0; s < len; s += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = (cv && s + u < len) ? ldhw(base + (s + u) * step, pol) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
+      xw[K - 1] = v[u];
+      double h = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) h = fma(w[i], xw[i], h);
+      const double h1 = std::is_same<IO, double>::value ? h : round_f32(h);
+      const double hc = (s + u < len) ? h1 - sh : 0.0;
+      S1 += hc;
+      S2 = fma(hc, hc, S2);
+    }
+  }
+}
+
+template <int K, typename IO, int U, int MODE, bool MULADD>
+__device__ __forceinline__ void fwd_pass2_piece(const IO* __restrict__ base, IO* __restrict__ obase, int64_t step,
+                                                int64_t s0, int64_t len, bool cv, const double (&wq)[K], double bf,
+                                                int skind, double alpha, uint64_t pol_in, uint64_t pol_out) {
+  double xw[K];
+#pragma unroll
+  for (int m = 1; m < K; ++m) {
+    const int64_t sp = s0 - K + m;
+    xw[m] = (cv && sp >= 0) ? ldhw(base + (int64_t)(m - K) * step, pol_in) : 0.0;
+  }
+  for (int64_t s = 0; s < len; s += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = (cv && s + u < len) ? ldhw(base + (s + u) * step, pol_in) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
+      xw[K - 1] = v[u];
+      double h = 0.0;
+      if (MULADD) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) h = __dadd_rn(h, __dmul_rn(wq[i], xw[i]));
+      } else {  // power-of-two weights: the product is exact, DFMA == mul then add
+#pragma unroll
+        for (int i = 0; i < K; ++i) h = fma(wq[i], xw[i], h);
+      }
+      h = __dadd_rn(h, bf);
+      if (cv && s + u < len) {
+        double o;
+        if (MODE == 1) {
+          const double h2 = std::is_same<IO, double>::value ? h : round_f32(h);
+          o = surrogate_primitive(skind, alpha, h2);
+        } else if (std::is_same<IO, double>::value) {
+          o = h >= 0.0 ? 1.0 : 0.0;
+        } else {
+          o = h >= -0x1p-150 ? 1.0 : 0.0;  // == (f32(h) >= 0)
+        }
+        sth(obase + (s + u) * step, o, pol_out);
+      }
+    }
+  }
+}
+
+// fold of one channel from the per-CTA shifted sums (one warp)
+__device__ void fwd_fold_channel(const FPlan& P, int64_t c, const double* __restrict__ part, const double* W,
+                                 int flags, const double* gamma, const double* beta, double* rm, double* rv,
+                                 double eps, double momentum, double* fold, int lane) {
+  const int K = P.k;
+  double S1 = 0.0, S2 = 0.0;
+  const int64_t total = (int64_t)P.nCTA * P.Q;
+  const int64_t plane = (int64_t)P.nCTA * P.J;
+  for (int64_t idx = lane; idx < total; idx += 32) {
+    const int64_t b = idx / P.Q, qq = idx - b * P.Q;
+    const int64_t o = b * P.J + c * P.Q + qq;
+    S1 += __ldcg(part + o);
+    S2 += __ldcg(part + plane + o);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double a1 = __shfl_xor_sync(0xffffffffu, S1, off);
+    const double a2 = __shfl_xor_sync(0xffffffffu, S2, off);
+    S1 = (lane & off) ? a1 + S1 : S1 + a1;
+    S2 = (lane & off) ? a2 + S2 : S2 + a2;
+  }
+  if (lane != 0) return;
+  const bool smooth = flags & PSN_SMOOTH;
+  const bool use_batch = flags & PSN_USE_BATCH_STATS;
+  const bool quantize = (flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH));
+  const double m = (double)(P.T * P.N * P.Q);
+  const double rm_prev = __ldcg(rm + c), rv_prev = __ldcg(rv + c);
+  const double dmean = S1 / m;
+  const double mu_b = rm_prev + dmean;  // the pass-1 shift was running_mean (pre-update)
+  double var_b = S2 / m - dmean * dmean;
+  var_b = var_b < 0.0 ? 0.0 : var_b;
+  if (!smooth) {  // network.py:241-248
+    const double unbiased = m > 1.0 ? var_b * (m / (m - 1.0)) : var_b;
+    double r1 = rm_prev * (1.0 - momentum);
+    r1 = r1 + momentum * mu_b;
+    double r2 = rv_prev * (1.0 - momentum);
+    r2 = r2 + momentum * unbiased;
+    rm[c] = r1;
+    rv[c] = r2;
+  }
+  const double mu = use_batch ? mu_b : rm_prev;
+  const double var = use_batch ? var_b : rv_prev;
+  const double s = sqrt(var + eps);
+  const double a = gamma[c] / s;
+  const double* Wc = W + ((flags & PSN_SHARED) ? 0 : c * K);
+  double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  f[0] = mu;
+  f[1] = s;
+  f[2] = a;
+  f[3] = beta[c] - a * mu;
+  f[4] = mu_b;
+  f[5] = var_b;
+  for (int i = 0; i < K; ++i) {
+    const double wf = a * Wc[i];
+    f[PSN_FOLD_HDR + i] = wf;
+    double wq = wf;
+    if (quantize) {
+      int sg, e;
+      quantize_pow2(wf, sg, e);
+      wq = ldexp((double)sg, e);
+    }
+    f[PSN_FOLD_HDR + K + i] = wq;
+  }
+  __threadfence();
+}
+
+template <int K, typename IO, int NW, int MODE, bool MULADD>
+__global__ void __launch_bounds__(NW * 32, 2)
+    fused_fwd_kernel(FPlan P, const IO* __restrict__ x, const double* __restrict__ W, const double* gamma,
+                     const double* beta, double* rm, double* rv, int flags, double eps, double momentum, int skind,
+                     double alpha, IO* __restrict__ out, double* fold, double* part, unsigned* ctr) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int wg = blockIdx.x * NW + wl;
+  const int tile = wg % P.NT;
+  const int slice = wg / P.NT;
+  const bool active = slice < P.S;
+  const int64_t rho0 = active ? (int64_t)slice * P.R / P.S : 0;
+  const int64_t rho1 = active ? (int64_t)(slice + 1) * P.R / P.S : 0;
+  const bool shared = flags & PSN_SHARED;
+  const int64_t step = (int64_t)P.d * P.row;
+  const int64_t plane = (int64_t)P.nCTA * P.J;
+  __shared__ double sred[2][NW][32];
+  const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+  const int iters = P.G + kLag;
+  for (int it = 0; it < iters; ++it) {
+    // ---------------- pass 1 of group `it`: shifted moments of h1 ----------
+    if (it < P.G) {
+      const int g = it;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int64_t colg = (int64_t)tile * 32 + lane;
+      const bool cv = active && colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + colg;
+      const int64_t c = cv ? col / P.Q : c0;
+      double w[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) w[i] = cv ? __ldg(W + (shared ? 0 : c * K) + i) : 0.0;
+      const double sh = cv ? __ldcg(rm + c) : 0.0;
+      double S1 = 0.0, S2 = 0.0;
+      for (int64_t rho = rho0; rho < rho1;) {
+        int64_t n, s, Sr;
+        int r;
+        row_decode(P, rho, n, r, s, Sr);
+        const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
+        const IO* base = x + (r + s * P.d) * P.row + n * P.J + col;
+        fwd_pass1_piece<K, IO, U>(base, step, s, len, cv, w, sh, S1, S2, pol_keep);
+        rho += len;
+      }
+      sred[0][wl][lane] = S1;
+      sred[1][wl][lane] = S2;
+      __syncthreads();
+      if (wl < P.NT) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int w2 = wl; w2 < NW; w2 += P.NT) {
+          a1 += sred[0][w2][lane];
+          a2 += sred[1][w2][lane];
+        }
+        const int64_t cg2 = (int64_t)wl * 32 + lane;
+        if (cg2 < (c1 - c0) * P.Q) {
+          const int64_t o = (int64_t)blockIdx.x * P.J + c0 * P.Q + cg2;
+          part[o] = a1;
+          part[plane + o] = a2;
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) red_release(ctr + 2 * g, 1u);
+    }
+    // ---------------- fold of group it-1 (one warp per channel) -----------
+    if (it >= 1 && it - 1 < P.G) {
+      const int g = it - 1;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int rot = (int)(((int64_t)g * 37) % P.nCTA);
+      int li = 0;
+      for (int64_t c = c0; c < c1; ++c) {
+        const int owner = (int)(((c - c0) + rot) % P.nCTA);
+        if (owner != (int)blockIdx.x) continue;
+        if ((li++ % NW) != wl) continue;
+        wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
+        fwd_fold_channel(P, c, part, W, flags, gamma, beta, rm, rv, eps, momentum, fold, lane);
+        __syncwarp();
+        if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
+      }
+    }
+    // ---------------- pass 2 of group it-kLag: spikes ----------------------
+    if (it >= kLag && it - kLag < P.G) {
+      const int g = it - kLag;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int64_t colg = (int64_t)tile * 32 + lane;
+      const bool cv = active && colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + colg;
+      const int64_t c = cv ? col / P.Q : c0;
+      if (active) wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+      double wq[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) wq[i] = cv ? __ldcg(f + PSN_FOLD_HDR + K + i) : 0.0;
+      const double bf = cv ? __ldcg(f + 3) : 0.0;
+      for (int64_t rho = rho0; rho < rho1;) {
+        int64_t n, s, Sr;
+        int r;
+        row_decode(P, rho, n, r, s, Sr);
+        const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
+        const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
+        fwd_pass2_piece<K, IO, U, MODE, MULADD>(x + off, out + off, step, s, len, cv, wq, bf, skind, alpha,
+                                                pol_drop, pol_drop);
+        rho += len;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// partials: [NV][nCTA][J] with NV = 3K+1: db, dwq[K], sx[K], sxc[K]
+// ---------------------------------------------------------------------------
+template <int K>
+struct BwdAcc {
+  double db, dwq[K], sxa, sxc[K], tail[K];
+};
+
+template <int K, typename IO, int U>
+__device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const IO* __restrict__ yb, int64_t step,
+                                                int64_t s0, int64_t len, int64_t Sr, bool cv, const float (&w)[K],
+                                                const float (&wq)[K], float bf, float mu, const Surrogate& sur,
+                                                BwdAcc<K>& A, uint64_t pol) {
+  float xw[K];
+#pragma unroll
+  for (int m = 1; m < K; ++m) {
+    const int64_t sp = s0 - K + m;
+    xw[m] = (cv && sp >= 0) ? ldh(xb + (int64_t)(m - K) * step, pol) : 0.0f;
+  }
+  for (int64_t s = 0; s < len; s += U) {
+    float xv[U], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = cv && s + u < len;
+      xv[u] = ok ? ldh(xb + (s + u) * step, pol) : 0.0f;
+      yv[u] = ok ? ldh(yb + (s + u) * step, pol) : 0.0f;
+    }
+    float fdb = 0.0f, fsa = 0.0f, fdw[K], fsc[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) fdw[i] = fsc[i] = 0.0f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
+      xw[K - 1] = xv[u];
+      float h1 = 0.0f, h2 = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        h1 = fmaf(w[i], xw[i], h1);
+        h2 = fmaf(wq[i], xw[i], h2);
+      }
+      h2 += bf;
+      const bool ok = s + u < len;
+      const float dh2 = ok ? yv[u] * surrogate_grad(sur, h2) : 0.0f;
+      const float hc = ok ? h1 - mu : 0.0f;
+      fdb += dh2;
+      fsa += xv[u];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        fdw[i] = fmaf(xw[i], dh2, fdw[i]);
+        fsc[i] = fmaf(xw[i], hc, fsc[i]);
+      }
+    }
+    A.db += (double)fdb;
+    A.sxa += (double)fsa;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      A.dwq[i] += (double)fdw[i];
+      A.sxc[i] += (double)fsc[i];
+    }
+  }
+  // Sx[i] = sum over t of x[t - off_i] excludes the last K-1-i steps of the stream
+  if (s0 + len == Sr && cv) {
+#pragma unroll
+    for (int dist = 0; dist < K - 1; ++dist) {
+      const int64_t p = len - 1 - dist;  // relative step, may precede this piece
+      if (s0 + p < 0) continue;
+      const float xv = ldh(xb + p * step, pol);
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i)
+        if (i < K - 1 - dist) A.tail[i] += (double)xv;
+    }
+  }
+}
+
+template <int K, typename IO, int U>
+__device__ __forceinline__ void bwd_passB_piece(const IO* __restrict__ xb, const IO* __restrict__ yb,
+                                                IO* __restrict__ ob, int64_t step, int64_t s0, int64_t len,
+                                                int64_t Sr, bool cv, const float (&w)[K], const float (&wq)[K],
+                                                float bf, float mu, float a1, float b1, const Surrogate& sur,
+                                                uint64_t pol_in, uint64_t pol_out) {
+  float xw[K], pacc[K];
+#pragma unroll
+  for (int m = 1; m < K; ++m) {
+    const int64_t sp = s0 - K + m;
+    xw[m] = (cv && sp >= 0) ? ldh(xb + (int64_t)(m - K) * step, pol_in) : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) pacc[i] = 0.0f;
+  const int64_t nsteps = len + K - 1;  // dh needed on [s0, s0+len+K-1) within the stream
+  for (int64_t s = 0; s < nsteps; s += U) {
+    float xv[U], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = cv && s + u < nsteps && s0 + s + u < Sr;
+      xv[u] = ok ? ldh(xb + (s + u) * step, pol_in) : 0.0f;
+      yv[u] = ok ? ldh(yb + (s + u) * step, pol_in) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
+      xw[K - 1] = xv[u];
+      float h1 = 0.0f, h2 = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        h1 = fmaf(w[i], xw[i], h1);
+        h2 = fmaf(wq[i], xw[i], h2);
+      }
+      h2 += bf;
+      const bool ok = s + u < nsteps && s0 + s + u < Sr;
+      const float dh2 = ok ? yv[u] * surrogate_grad(sur, h2) : 0.0f;
+      const float dh1 = ok ? fmaf(b1, h1 - mu, a1) : 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        pacc[i] = fmaf(wq[i], dh2, pacc[i]);
+        pacc[i] = fmaf(w[i], dh1, pacc[i]);
+      }
+      const int64_t o = s + u - (K - 1);
+      if (cv && o >= 0 && o < len) sth(ob + o * step, (double)pacc[0], pol_out);
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) pacc[i] = pacc[i + 1];
+      pacc[K - 1] = 0.0f;
+    }
+  }
+}
+
+__device__ void bwd_fold_channel(const FPlan& P, int64_t c, const double* __restrict__ part, const double* W,
+                                 int flags, const double* gamma, const double* fold, double* dW, double* dgamma,
+                                 double* dbeta, double* bfold, int lane) {
+  const int K = P.k;
+  const int NV = 3 * K + 1;
+  const int64_t total = (int64_t)P.nCTA * P.Q;
+  const int64_t plane = (int64_t)P.nCTA * P.J;
+  double tot[3 * PSN_MAX_ORDER + 1];
+  for (int v = 0; v < NV; ++v) {
+    double acc = 0.0;
+    for (int64_t idx = lane; idx < total; idx += 32) {
+      const int64_t b = idx / P.Q, qq = idx - b * P.Q;
+      acc += __ldcg(part + v * plane + b * P.J + c * P.Q + qq);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, acc, off);
+      acc = (lane & off) ? o + acc : acc + o;
+    }
+    tot[v] = acc;
+  }
+  if (lane != 0) return;
+  const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  const double mu = f[0], s = f[1], a = f[2];
+  const bool quantized = (flags & PSN_QUANTIZED) && (!(flags & PSN_SMOOTH) || (flags & PSN_QUANTIZE_IN_SMOOTH));
+  const double* Wc = W + ((flags & PSN_SHARED) ? 0 : c * K);
+  const double db_f = tot[0];
+  double da = 0.0;
+  double dwf[PSN_MAX_ORDER];
+  for (int i = 0; i < K; ++i) {
+    double g1 = tot[1 + i];
+    if (quantized && (flags & PSN_ROUND_STE)) {
+      const double wf = f[PSN_FOLD_HDR + i], wq = f[PSN_FOLD_HDR + K + i];
+      g1 = (wf != 0.0) ? g1 * (fabs(wq) / fabs(wf)) : 0.0;
+    }
+    dwf[i] = g1;
+    da = da + dwf[i] * Wc[i];
+  }
+  da = da - db_f * mu;
+  double alpha1 = 0.0, beta1 = 0.0;
+  if (flags & PSN_USE_BATCH_STATS) {
+    const double m = (double)(P.T * P.N * P.Q);
+    const double ds = -da * gamma[c] / (s * s);
+    const double dvar = ds / (2.0 * s);
+    const double dmu = -db_f * a;
+    alpha1 = dmu / m;
+    beta1 = (2.0 / m) * dvar;
+  }
+  for (int i = 0; i < K; ++i) {
+    double dw = a * dwf[i];
+    if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * tot[1 + K + i] + beta1 * tot[1 + 2 * K + i];
+    dW[c * K + i] = dw;
+  }
+  dbeta[c] = db_f;
+  dgamma[c] = da / s;
+  bfold[2 * c] = alpha1;
+  bfold[2 * c + 1] = beta1;
+  __threadfence();
+}
+
+template <int K, typename IO, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    fused_bwd_kernel(FPlan P, const IO* __restrict__ x, const IO* __restrict__ dy, const double* __restrict__ W,
+                     const double* gamma, const double* fold, int flags, Surrogate sur, IO* __restrict__ dx,
+                     double* dW, double* dgamma, double* dbeta, double* bfold, double* part, unsigned* ctr) {
+  constexpr int U = 8;
+  const int NV = 3 * K + 1;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int wg = blockIdx.x * NW + wl;
+  const int tile = wg % P.NT;
+  const int slice = wg / P.NT;
+  const bool active = slice < P.S;
+  const int64_t rho0 = active ? (int64_t)slice * P.R / P.S : 0;
+  const int64_t rho1 = active ? (int64_t)(slice + 1) * P.R / P.S : 0;
+  const bool shared = flags & PSN_SHARED;
+  const int64_t step = (int64_t)P.d * P.row;
+  const int64_t plane = (int64_t)P.nCTA * P.J;
+  __shared__ double sred[4][NW][32];
+  const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+  const int iters = P.G + kLag;
+  for (int it = 0; it < iters; ++it) {
+    // ---------------- pass A of group `it`: per-column sums ----------------
+    if (it < P.G) {
+      const int g = it;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int64_t colg = (int64_t)tile * 32 + lane;
+      const bool cv = active && colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + colg;
+      const int64_t c = cv ? col / P.Q : c0;
+      const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+      float w[K], wq[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        w[i] = cv ? (float)__ldg(W + (shared ? 0 : c * K) + i) : 0.0f;
+        wq[i] = cv ? (float)__ldg(f + PSN_FOLD_HDR + K + i) : 0.0f;
+      }
+      const float bf = cv ? (float)__ldg(f + 3) : 0.0f;
+      const float mu = cv ? (float)__ldg(f + 0) : 0.0f;
+      BwdAcc<K> A;
+      A.db = A.sxa = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) A.dwq[i] = A.sxc[i] = A.tail[i] = 0.0;
+      for (int64_t rho = rho0; rho < rho1;) {
+        int64_t n, s, Sr;
+        int r;
+        row_decode(P, rho, n, r, s, Sr);
+        const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
+        const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
+        bwd_passA_piece<K, IO, U>(x + off, dy + off, step, s, len, Sr, cv, w, wq, bf, mu, sur, A, pol_keep);
+        rho += len;
+      }
+      // CTA reduction, 4 values per round, then one partial per (CTA, column)
+      for (int v0 = 0; v0 < NV; v0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int v = v0 + u;
+          double val = 0.0;
+          if (v == 0) val = A.db;
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            if (v == 1 + i) val = A.dwq[i];
+            if (v == 1 + K + i) val = A.sxa - (i < K - 1 ? A.tail[i] : 0.0);
+            if (v == 1 + 2 * K + i) val = A.sxc[i];
+          }
+          sred[u][wl][lane] = val;
+        }
+        __syncthreads();
+        if (wl < P.NT) {
+          const int64_t cg2 = (int64_t)wl * 32 + lane;
+          const bool ok = cg2 < (c1 - c0) * P.Q;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int v = v0 + u;
+            if (v < NV) {
+              double a = 0.0;
+              for (int w2 = wl; w2 < NW; w2 += P.NT) a += sred[u][w2][lane];
+              if (ok) part[v * plane + (int64_t)blockIdx.x * P.J + c0 * P.Q + cg2] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (wl < P.NT) __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) red_release(ctr + 2 * g, 1u);
+    }
+    // ---------------- fold of group it-1 ------------------------------------
+    if (it >= 1 && it - 1 < P.G) {
+      const int g = it - 1;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int rot = (int)(((int64_t)g * 37) % P.nCTA);
+      int li = 0;
+      for (int64_t c = c0; c < c1; ++c) {
+        const int owner = (int)(((c - c0) + rot) % P.nCTA);
+        if (owner != (int)blockIdx.x) continue;
+        if ((li++ % NW) != wl) continue;
+        wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
+        bwd_fold_channel(P, c, part, W, flags, gamma, fold, dW, dgamma, dbeta, bfold, lane);
+        __syncwarp();
+        if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
+      }
+    }
+    // ---------------- pass B of group it-kLag: dx --------------------------
+    if (it >= kLag && it - kLag < P.G) {
+      const int g = it - kLag;
+      const int64_t c0 = (int64_t)g * P.cpg;
+      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      const int64_t colg = (int64_t)tile * 32 + lane;
+      const bool cv = active && colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + colg;
+      const int64_t c = cv ? col / P.Q : c0;
+      if (active) wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+      float w[K], wq[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        w[i] = cv ? (float)__ldg(W + (shared ? 0 : c * K) + i) : 0.0f;
+        wq[i] = cv ? (float)__ldg(f + PSN_FOLD_HDR + K + i) : 0.0f;
+      }
+      const float bf = cv ? (float)__ldg(f + 3) : 0.0f;
+      const float mu = cv ? (float)__ldg(f + 0) : 0.0f;
+      const float a1 = cv ? (float)__ldcg(bfold + 2 * c) : 0.0f;
+      const float b1 = cv ? (float)__ldcg(bfold + 2 * c + 1) : 0.0f;
+      for (int64_t rho = rho0; rho < rho1;) {
+        int64_t n, s, Sr;
+        int r;
+        row_decode(P, rho, n, r, s, Sr);
+        const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
+        const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
+        bwd_passB_piece<K, IO, U>(x + off, dy + off, dx + off, step, s, len, Sr, cv, w, wq, bf, mu, a1, b1, sur,
+                                  pol_drop, pol_drop);
+        rho += len;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+constexpr int kFwdNW = 16;  // 512 threads, 2 CTAs per SM
+constexpr int kBwdNW = 16;  // 512 threads, 1 CTA per SM
+constexpr int kFwdCtasPerSm = 2;
+constexpr int kBwdCtasPerSm = 1;
+
+static int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+static double group_bytes_budget() {
+  const char* e = getenv("PSN_GROUP_MB");
+  const double mb = e ? atof(e) : 16.0;
+  return (mb > 0 ? mb : 16.0) * 1e6;
+}
+
+// returns false when the fused path does not cover the shape (generic path then)
+bool fused_plan(const psn_desc_t* desc, bool backward, FPlan& P) {
+  const int NW = backward ? kBwdNW : kFwdNW;
+  if (getenv("PSN_FORCE_GENERIC")) return false;
+  if (desc->k > 8) return false;                  // larger orders: generic path
+  if (desc->Q != 1) return false;                 // spatial inputs: generic path (per-column partials)
+  if (backward && desc->dtype == PSN_F64) return false;  // f64 carrier keeps the f64 generic backward
+  const int esize = (int)dtype_size(desc->dtype);
+  P.T = desc->T;
+  P.N = desc->N;
+  P.C = desc->C;
+  P.Q = desc->Q;
+  P.J = P.C * P.Q;
+  P.row = P.N * P.J;
+  P.R = P.N * P.T;
+  P.d = desc->d;
+  P.k = desc->k;
+  P.q = (int)(P.T / P.d);
+  P.m = (int)(P.T % P.d);
+  P.NW = NW;
+  P.nCTA = num_sms() * (backward ? kBwdCtasPerSm : kFwdCtasPerSm);
+  const double per_col = (double)P.T * P.N * esize * (backward ? 2 : 1);
+  double target_cols = group_bytes_budget() / per_col;
+  int NT = 1;
+  while (NT < NW && 32.0 * NT < target_cols) NT <<= 1;
+  while (NT < NW && 32 * NT < P.Q) NT <<= 1;
+  if (32 * NT < P.Q) return false;
+  int64_t cpg = (32 * (int64_t)NT) / P.Q;
+  if (cpg > P.C) cpg = P.C;
+  // shrink the tile count when the whole layer is smaller than one group
+  while (NT > 1 && 32 * (NT / 2) >= cpg * P.Q) NT >>= 1;
+  P.NT = NT;
+  P.cpg = cpg;
+  P.G = (int)((P.C + cpg - 1) / cpg);
+  P.S = (P.nCTA * NW) / NT;
+  if (P.S > P.R) P.S = (int)P.R;
+  return P.G <= 4096;
+}
+
+size_t fused_workspace_bytes(const psn_desc_t* desc) {
+  size_t need = 0;
+  for (int b = 0; b < 2; ++b) {
+    FPlan P;
+    if (!fused_plan(desc, b == 1, P)) continue;
+    const size_t nv = b ? 3 * (size_t)P.k + 1 : 2;
+    size_t bytes = 256 + 8 * (2 * (size_t)P.G) + 8 * nv * (size_t)P.nCTA * P.J + 16 * (size_t)P.C + 1024;
+    if (bytes > need) need = bytes;
+  }
+  return need;
+}
+
+struct FusedWs {
+  unsigned* ctr;
+  double* part;
+  double* bfold;
+};
+
+static FusedWs carve(void* ws, const FPlan& P) {
+  FusedWs w;
+  char* p = (char*)ws;
+  w.ctr = (unsigned*)p;
+  size_t off = ((size_t)2 * P.G * sizeof(unsigned) + 255) & ~(size_t)255;
+  w.bfold = (double*)(p + off);
+  off += ((size_t)16 * P.C + 255) & ~(size_t)255;
+  w.part = (double*)(p + off);
+  return w;
+}
+
+// co-resident CTAs of a kernel instance (cooperative launch needs all of them)
+template <typename F>
+static int resident_ctas(F kernel, int block) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel, block, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return per_sm * num_sms();
+}
+
+static void fit_grid(FPlan& P, int resident) {
+  if (resident > 0 && resident < P.nCTA) P.nCTA = resident;
+  P.S = (P.nCTA * P.NW) / P.NT;
+  if (P.S > P.R) P.S = (int)P.R;
+}
+
+template <typename F>
+static int coop_launch(F kernel, FPlan& P, int block, void** args, cudaStream_t st) {
+  fit_grid(P, resident_ctas(kernel, block));
+  const int grid = P.nCTA;
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, 0, st);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(PSN_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return PSN_OK;
+}
+
+template <int K, typename IO>
+int fused_forward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, const double* W, const double* gamma,
+                    const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
+  FPlan P = Pin;
+  FusedWs w = carve(ws, P);
+  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * P.G, st) != cudaSuccess)
+    return fail(PSN_ERR_CUDA, "memset of fused counters failed");
+  int flags = desc->flags;
+  double eps = desc->eps, mom = desc->momentum, alpha = desc->alpha;
+  int skind = desc->surrogate;
+  const IO* xp = (const IO*)x;
+  IO* op = (IO*)out;
+  void* args[] = {&P, &xp, (void*)&W, (void*)&gamma, (void*)&beta, &rm, &rv, &flags, &eps, &mom, &skind,
+                  &alpha, &op, &fold, &w.part, &w.ctr};
+  const bool smooth = flags & PSN_SMOOTH;
+  const bool muladd = !((flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH)));
+  if (smooth) {
+    if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, true>, P, kFwdNW * 32, args, st);
+    return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, false>, P, kFwdNW * 32, args, st);
+  }
+  if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, true>, P, kFwdNW * 32, args, st);
+  return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, false>, P, kFwdNW * 32, args, st);
+}
+
+template <int K, typename IO>
+int fused_backward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, const void* dy, const double* W,
+                     const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
+                     double* dwtmp, void* ws, cudaStream_t st) {
+  FPlan P = Pin;
+  FusedWs w = carve(ws, P);
+  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * P.G, st) != cudaSuccess)
+    return fail(PSN_ERR_CUDA, "memset of fused counters failed");
+  int flags = desc->flags;
+  const bool shared = flags & PSN_SHARED;
+  Surrogate sur;
+  sur.kind = desc->surrogate;
+  if (desc->surrogate == PSN_ARCTAN) {
+    sur.c = (float)(0.5 * 3.141592653589793 * desc->alpha);
+    sur.scale = (float)(desc->alpha / 2.0);
+  } else {
+    sur.c = (float)desc->alpha;
+    sur.scale = 1.0f;
+  }
+  const IO* xp = (const IO*)x;
+  const IO* yp = (const IO*)dy;
+  IO* op = (IO*)dx;
+  double* dWp = shared ? dwtmp : dW;
+  void* args[] = {&P, &xp, &yp, (void*)&W, (void*)&gamma, (void*)&fold, &flags, &sur, &op, &dWp, &dgamma,
+                  &dbeta, &w.bfold, &w.part, &w.ctr};
+  return coop_launch(fused_bwd_kernel<K, IO, kBwdNW>, P, kBwdNW * 32, args, st);
+}
+
+#define PSN_FK_CASES(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
+#define PSN_BK_CASES(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
+
+template <typename IO>
+int fused_forward_dt(const psn_desc_t* desc, const FPlan& P, const void* x, const double* W, const double* gamma,
+                     const double* beta, double* rm, double* rv, void* out, double* fold, void* ws,
+                     cudaStream_t st) {
+  switch (desc->k) {
+#define C_(KK) \
+  case KK:     \
+    return fused_forward_k<KK, IO>(desc, P, x, W, gamma, beta, rm, rv, out, fold, ws, st);
+    PSN_FK_CASES(C_)
+#undef C_
+  }
+  return fail(PSN_ERR_ORDER, "order out of range for the fused forward");
+}
+
+template <typename IO>
+int fused_backward_dt(const psn_desc_t* desc, const FPlan& P, const void* x, const void* dy, const double* W,
+                      const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
+                      double* dwtmp, void* ws, cudaStream_t st) {
+  switch (desc->k) {
+#define C_(KK) \
+  case KK:     \
+    return fused_backward_k<KK, IO>(desc, P, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, dwtmp, ws, st);
+    PSN_BK_CASES(C_)
+#undef C_
+  }
+  return fail(PSN_ERR_ORDER, "order out of range for the fused backward");
+}
+
+int fused_forward(const psn_desc_t* desc, const FPlan& P, const void* x, const double* W, const double* gamma,
+                  const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
+  switch (desc->dtype) {
+    case PSN_F32:
+      return fused_forward_dt<float>(desc, P, x, W, gamma, beta, rm, rv, out, fold, ws, st);
+    case PSN_BF16:
+      return fused_forward_dt<__nv_bfloat16>(desc, P, x, W, gamma, beta, rm, rv, out, fold, ws, st);
+    case PSN_F64:
+      return fused_forward_dt<double>(desc, P, x, W, gamma, beta, rm, rv, out, fold, ws, st);
+  }
+  return fail(PSN_ERR_DTYPE, "unsupported carrier dtype");
+}
+
+int fused_backward(const psn_desc_t* desc, const FPlan& P, const void* x, const void* dy, const double* W,
+                   const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
+                   double* dwtmp, void* ws, cudaStream_t st) {
+  switch (desc->dtype) {
+    case PSN_F32:
+      return fused_backward_dt<float>(desc, P, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, dwtmp, ws, st);
+    case PSN_BF16:
+      return fused_backward_dt<__nv_bfloat16>(desc, P, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, dwtmp, ws,
+                                              st);
+  }
+  return fail(PSN_ERR_DTYPE, "unsupported carrier dtype");
+}
+
+}  // namespace psn
+
+extern "C" int psn_plan_info(const psn_desc_t* desc, int backward, int64_t* info, int n) {
+  using namespace psn;
+  if (!desc || !info || n <= 0 || validate(desc, false) != PSN_OK) return 0;
+  int64_t v[6] = {0, 0, 0, 0, 0, 3};
+  FPlan P;
+  if (fused_plan(desc, backward != 0, P)) {
+    // the launch may shrink the grid to the co-resident CTA count; report the plan
+    v[0] = 1;
+    v[1] = P.nCTA;
+    v[2] = P.G;
+    v[3] = P.NT;
+    v[4] = P.S;
+    v[5] = 2 + ((backward && (desc->flags & PSN_SHARED)) ? 1 : 0);
+  } else {
+    v[5] = 3 + ((backward && (desc->flags & PSN_SHARED)) ? 1 : 0);
+  }
+  const int m = n < 6 ? n : 6;
+  for (int i = 0; i < m; ++i) info[i] = v[i];
+  return m;
+}

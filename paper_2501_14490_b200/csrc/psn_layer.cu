@@ -76,7 +76,7 @@ Geom plan(const psn_desc_t* desc) {
 }
 
 struct WsLayout {
-  size_t part1, part3, bfold, dwtmp, evalfold, total;
+  size_t part1, part3, bfold, dwtmp, evalfold, fused, total;
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -95,6 +95,8 @@ WsLayout ws_layout(const psn_desc_t* desc) {
   off = align256(off + sizeof(double) * (size_t)g.k * g.C);
   w.evalfold = off;
   off = align256(off + sizeof(double) * (PSN_FOLD_HDR + 2 * (size_t)g.k) * g.C);
+  w.fused = off;
+  off = align256(off + fused_workspace_bytes(desc));
   w.total = off;
   return w;
 }
@@ -794,6 +796,12 @@ int psn_forward_train(const psn_desc_t* desc, const void* x, const double* W, co
     return rc;
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
+  FPlan P;
+  if (fused_plan(desc, false, P)) {
+    rc = fused_forward(desc, P, x, W, gamma, beta, running_mean, running_var, out, fold,
+                       (char*)workspace + L.fused, (cudaStream_t)stream);
+    return rc ? rc : cuda_check("psn_forward_train (fused)");
+  }
   return by_dtype_k<FwdOp>(desc, desc, g, x, W, gamma, beta, running_mean, running_var, out, fold,
                            (char*)workspace, L, (cudaStream_t)stream);
 }
@@ -811,6 +819,15 @@ int psn_backward(const psn_desc_t* desc, const void* x, const void* dy, const do
     return rc;
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
+  FPlan P;
+  if (fused_plan(desc, true, P)) {
+    double* dwtmp = (double*)((char*)workspace + L.dwtmp);
+    rc = fused_backward(desc, P, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, dwtmp,
+                        (char*)workspace + L.fused, (cudaStream_t)stream);
+    if (rc) return rc;
+    if (desc->flags & PSN_SHARED) shared_rowsum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dwtmp, desc->C, desc->k, dW);
+    return cuda_check("psn_backward (fused)");
+  }
   return by_dtype_k<BwdOp>(desc, desc, g, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, (char*)workspace, L,
                            (cudaStream_t)stream);
 }
