@@ -90,8 +90,19 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
 __device__ __forceinline__ void red_release(unsigned* a, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+// poll with relaxed loads (no L1 invalidation per poll), then one acquire fence
 __device__ __forceinline__ void wait_geq(const unsigned* a, unsigned target) {
-  while (ld_acquire(a) < target) __nanosleep(64);
+  if (ld_relaxed(a) < target) {
+    do {
+      __nanosleep(32);
+    } while (ld_relaxed(a) < target);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // f32 rounding of an f64 value with two DADDs (exact (double)(float)h for every
@@ -214,13 +225,21 @@ __device__ void fwd_fold_channel(const FPlan& P, int64_t c, const double* __rest
                                  double eps, double momentum, double* fold, int lane) {
   const int K = P.k;
   double S1 = 0.0, S2 = 0.0;
-  const int64_t total = (int64_t)P.nCTA * P.Q;
   const int64_t plane = (int64_t)P.nCTA * P.J;
-  for (int64_t idx = lane; idx < total; idx += 32) {
-    const int64_t b = idx / P.Q, qq = idx - b * P.Q;
-    const int64_t o = b * P.J + c * P.Q + qq;
-    S1 += __ldcg(part + o);
-    S2 += __ldcg(part + plane + o);
+  for (int b0 = 0; b0 < P.nCTA; b0 += 4 * 32) {  // 4 independent loads in flight per lane
+    double v1[4], v2[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int b = b0 + lane + 32 * t;
+      const bool ok = b < P.nCTA;
+      v1[t] = ok ? __ldcg(part + (int64_t)b * P.J + c) : 0.0;
+      v2[t] = ok ? __ldcg(part + plane + (int64_t)b * P.J + c) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      S1 += v1[t];
+      S2 += v2[t];
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -275,7 +294,7 @@ __device__ void fwd_fold_channel(const FPlan& P, int64_t c, const double* __rest
 }
 
 template <int K, typename IO, int NW, int MODE, bool MULADD>
-__global__ void __launch_bounds__(NW * 32, 2)
+__global__ void __launch_bounds__(NW * 32, 1)
     fused_fwd_kernel(FPlan P, const IO* __restrict__ x, const double* __restrict__ W, const double* gamma,
                      const double* beta, double* rm, double* rv, int flags, double eps, double momentum, int skind,
                      double alpha, IO* __restrict__ out, double* fold, double* part, unsigned* ctr) {
@@ -343,11 +362,10 @@ __global__ void __launch_bounds__(NW * 32, 2)
       const int64_t c0 = (int64_t)g * P.cpg;
       const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
       const int rot = (int)(((int64_t)g * 37) % P.nCTA);
+      const int first = ((int)blockIdx.x - rot + P.nCTA) % P.nCTA;
       int li = 0;
-      for (int64_t c = c0; c < c1; ++c) {
-        const int owner = (int)(((c - c0) + rot) % P.nCTA);
-        if (owner != (int)blockIdx.x) continue;
-        if ((li++ % NW) != wl) continue;
+      for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
+        if ((li % NW) != wl) continue;
         wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
         fwd_fold_channel(P, c, part, W, flags, gamma, beta, rm, rv, eps, momentum, fold, lane);
         __syncwarp();
@@ -392,16 +410,45 @@ struct BwdAcc {
   double db, dwq[K], sxa, sxc[K], tail[K];
 };
 
+// f64 surrogate derivative (reference surrogate.py:36-38) on the f32-rounded h2
+struct SurD {
+  int kind;
+  double c;      // arctan: 0.5*pi*alpha ; rational: alpha
+  double scale;  // arctan: alpha/2       ; rational: 1
+};
+
+__device__ __forceinline__ double rcp_f64(double v) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  double e = fma(-v, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-v, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double surrogate_grad_f64(const SurD& sd, double h) {
+  const double u = sd.c * h;
+  const double den = sd.kind == PSN_ARCTAN ? fma(u, u, 1.0) : fma(u, h, 1.0);
+  return sd.scale * rcp_f64(den);
+}
+
+// pass A: h2 is recomputed exactly (f64, reference tap order, f32-rounded like
+// the reference's carrier) so sigma'(h2) sees the reference's input; dh2 and
+// the per-channel sums db, dw_q are f64 — per-element f32 errors would grow
+// ~sqrt(m) in these m-term reductions.  The BN-term sums (sx, sxc) only reach
+// dW through the 1/m-scaled alpha1/beta1 and use f32 within a batch.
 template <int K, typename IO, int U>
 __device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const IO* __restrict__ yb, int64_t step,
                                                 int64_t s0, int64_t len, int64_t Sr, bool cv, const float (&w)[K],
-                                                const float (&wq)[K], float bf, float mu, const Surrogate& sur,
+                                                const double (&wqd)[K], double bfd, float mu, const SurD& sd,
                                                 BwdAcc<K>& A, uint64_t pol) {
   float xw[K];
+  double xwd[K];
 #pragma unroll
   for (int m = 1; m < K; ++m) {
     const int64_t sp = s0 - K + m;
     xw[m] = (cv && sp >= 0) ? ldh(xb + (int64_t)(m - K) * step, pol) : 0.0f;
+    xwd[m] = (double)xw[m];
   }
   for (int64_t s = 0; s < len; s += U) {
     float xv[U], yv[U];
@@ -411,39 +458,39 @@ __device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const
       xv[u] = ok ? ldh(xb + (s + u) * step, pol) : 0.0f;
       yv[u] = ok ? ldh(yb + (s + u) * step, pol) : 0.0f;
     }
-    float fdb = 0.0f, fsa = 0.0f, fdw[K], fsc[K];
+    float fsa = 0.0f, fsc[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) fdw[i] = fsc[i] = 0.0f;
+    for (int i = 0; i < K; ++i) fsc[i] = 0.0f;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
-      for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
-      xw[K - 1] = xv[u];
-      float h1 = 0.0f, h2 = 0.0f;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        h1 = fmaf(w[i], xw[i], h1);
-        h2 = fmaf(wq[i], xw[i], h2);
+      for (int i = 0; i < K - 1; ++i) {
+        xw[i] = xw[i + 1];
+        xwd[i] = xwd[i + 1];
       }
-      h2 += bf;
+      xw[K - 1] = xv[u];
+      xwd[K - 1] = (double)xv[u];
+      double h = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) h = fma(wqd[i], xwd[i], h);
+      h = __dadd_rn(h, bfd);
+      const double h2 = std::is_same<IO, double>::value ? h : round_f32(h);
       const bool ok = s + u < len;
-      const float dh2 = ok ? yv[u] * surrogate_grad(sur, h2) : 0.0f;
+      const double dh2 = ok ? (double)yv[u] * surrogate_grad_f64(sd, h2) : 0.0;
+      A.db += dh2;
+#pragma unroll
+      for (int i = 0; i < K; ++i) A.dwq[i] = fma(xwd[i], dh2, A.dwq[i]);
+      float h1 = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) h1 = fmaf(w[i], xw[i], h1);
       const float hc = ok ? h1 - mu : 0.0f;
-      fdb += dh2;
       fsa += xv[u];
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        fdw[i] = fmaf(xw[i], dh2, fdw[i]);
-        fsc[i] = fmaf(xw[i], hc, fsc[i]);
-      }
+      for (int i = 0; i < K; ++i) fsc[i] = fmaf(xw[i], hc, fsc[i]);
     }
-    A.db += (double)fdb;
     A.sxa += (double)fsa;
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      A.dwq[i] += (double)fdw[i];
-      A.sxc[i] += (double)fsc[i];
-    }
+    for (int i = 0; i < K; ++i) A.sxc[i] += (double)fsc[i];
   }
   // Sx[i] = sum over t of x[t - off_i] excludes the last K-1-i steps of the stream
   if (s0 + len == Sr && cv) {
@@ -516,14 +563,19 @@ __device__ void bwd_fold_channel(const FPlan& P, int64_t c, const double* __rest
                                  double* dbeta, double* bfold, int lane) {
   const int K = P.k;
   const int NV = 3 * K + 1;
-  const int64_t total = (int64_t)P.nCTA * P.Q;
   const int64_t plane = (int64_t)P.nCTA * P.J;
   double tot[3 * PSN_MAX_ORDER + 1];
   for (int v = 0; v < NV; ++v) {
     double acc = 0.0;
-    for (int64_t idx = lane; idx < total; idx += 32) {
-      const int64_t b = idx / P.Q, qq = idx - b * P.Q;
-      acc += __ldcg(part + v * plane + b * P.J + c * P.Q + qq);
+    for (int b0 = 0; b0 < P.nCTA; b0 += 4 * 32) {
+      double vv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int b = b0 + lane + 32 * t;
+        vv[t] = b < P.nCTA ? __ldcg(part + v * plane + (int64_t)b * P.J + c) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc += vv[t];
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -574,7 +626,8 @@ __device__ void bwd_fold_channel(const FPlan& P, int64_t c, const double* __rest
 template <int K, typename IO, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     fused_bwd_kernel(FPlan P, const IO* __restrict__ x, const IO* __restrict__ dy, const double* __restrict__ W,
-                     const double* gamma, const double* fold, int flags, Surrogate sur, IO* __restrict__ dx,
+                     const double* gamma, const double* fold, int flags, Surrogate sur, SurD sd,
+                     IO* __restrict__ dx,
                      double* dW, double* dgamma, double* dbeta, double* bfold, double* part, unsigned* ctr) {
   constexpr int U = 8;
   const int NV = 3 * K + 1;
@@ -602,13 +655,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const int64_t col = c0 * P.Q + colg;
       const int64_t c = cv ? col / P.Q : c0;
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
-      float w[K], wq[K];
+      float w[K];
+      double wqd[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         w[i] = cv ? (float)__ldg(W + (shared ? 0 : c * K) + i) : 0.0f;
-        wq[i] = cv ? (float)__ldg(f + PSN_FOLD_HDR + K + i) : 0.0f;
+        wqd[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;
       }
-      const float bf = cv ? (float)__ldg(f + 3) : 0.0f;
+      const double bfd = cv ? __ldg(f + 3) : 0.0;
       const float mu = cv ? (float)__ldg(f + 0) : 0.0f;
       BwdAcc<K> A;
       A.db = A.sxa = 0.0;
@@ -620,7 +674,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         row_decode(P, rho, n, r, s, Sr);
         const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
         const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
-        bwd_passA_piece<K, IO, U>(x + off, dy + off, step, s, len, Sr, cv, w, wq, bf, mu, sur, A, pol_keep);
+        bwd_passA_piece<K, IO, U>(x + off, dy + off, step, s, len, Sr, cv, w, wqd, bfd, mu, sd, A, pol_keep);
         rho += len;
       }
       // CTA reduction, 4 values per round, then one partial per (CTA, column)
@@ -664,11 +718,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const int64_t c0 = (int64_t)g * P.cpg;
       const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
       const int rot = (int)(((int64_t)g * 37) % P.nCTA);
+      const int first = ((int)blockIdx.x - rot + P.nCTA) % P.nCTA;
       int li = 0;
-      for (int64_t c = c0; c < c1; ++c) {
-        const int owner = (int)(((c - c0) + rot) % P.nCTA);
-        if (owner != (int)blockIdx.x) continue;
-        if ((li++ % NW) != wl) continue;
+      for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
+        if ((li % NW) != wl) continue;
         wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
         bwd_fold_channel(P, c, part, W, flags, gamma, fold, dW, dgamma, dbeta, bfold, lane);
         __syncwarp();
@@ -713,9 +766,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-constexpr int kFwdNW = 16;  // 512 threads, 2 CTAs per SM
+constexpr int kFwdNW = 32;  // 1024 threads, 1 CTA per SM
 constexpr int kBwdNW = 16;  // 512 threads, 1 CTA per SM
-constexpr int kFwdCtasPerSm = 2;
+constexpr int kFwdCtasPerSm = 1;
 constexpr int kBwdCtasPerSm = 1;
 
 static int num_sms() {
@@ -873,8 +926,17 @@ int fused_backward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, co
   const IO* xp = (const IO*)x;
   const IO* yp = (const IO*)dy;
   IO* op = (IO*)dx;
+  SurD sd;
+  sd.kind = desc->surrogate;
+  if (desc->surrogate == PSN_ARCTAN) {
+    sd.c = 0.5 * 3.141592653589793 * desc->alpha;
+    sd.scale = desc->alpha / 2.0;
+  } else {
+    sd.c = desc->alpha;
+    sd.scale = 1.0;
+  }
   double* dWp = shared ? dwtmp : dW;
-  void* args[] = {&P, &xp, &yp, (void*)&W, (void*)&gamma, (void*)&fold, &flags, &sur, &op, &dWp, &dgamma,
+  void* args[] = {&P, &xp, &yp, (void*)&W, (void*)&gamma, (void*)&fold, &flags, &sur, &sd, &op, &dWp, &dgamma,
                   &dbeta, &w.bfold, &w.part, &w.ctr};
   return coop_launch(fused_bwd_kernel<K, IO, kBwdNW>, P, kBwdNW * 32, args, st);
 }
