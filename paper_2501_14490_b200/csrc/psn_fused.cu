@@ -82,6 +82,69 @@ __device__ __forceinline__ void sth(__nv_bfloat16* a, double v, uint64_t pol) {
 }
 __device__ __forceinline__ void sth(float* a, double v, uint64_t pol) { sth(a, (float)v, pol); }
 
+// predicated (branch-free) variants: the load returns 0 and the store is
+// skipped when ok == false; no control flow, so unrolled batches stay one
+// basic block and the register windows are renamed instead of moved
+__device__ __forceinline__ float ldp(const float* a, uint64_t pol, bool ok) {
+  float v;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tmov.b32 %0, 0;\n\t"
+      "@p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n\t}"
+      : "=f"(v) : "l"(a), "l"(pol), "r"((int)ok));
+  return v;
+}
+__device__ __forceinline__ float ldp(const __nv_bfloat16* a, uint64_t pol, bool ok) {
+  unsigned short v;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tmov.b16 %0, 0;\n\t"
+      "@p ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;\n\t}"
+      : "=h"(v) : "l"(a), "l"(pol), "r"((int)ok));
+  return __uint_as_float(((unsigned)v) << 16);
+}
+__device__ __forceinline__ double ldpw(const double* a, uint64_t pol, bool ok) {
+  double v;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tmov.b64 %0, 0;\n\t"
+      "@p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n\t}"
+      : "=d"(v) : "l"(a), "l"(pol), "r"((int)ok));
+  return v;
+}
+__device__ __forceinline__ float ldp(const double* a, uint64_t pol, bool ok) { return (float)ldpw(a, pol, ok); }
+__device__ __forceinline__ double ldpw(const float* a, uint64_t pol, bool ok) { return (double)ldp(a, pol, ok); }
+__device__ __forceinline__ double ldpw(const __nv_bfloat16* a, uint64_t pol, bool ok) {
+  return (double)ldp(a, pol, ok);
+}
+__device__ __forceinline__ void stp(float* a, double v, uint64_t pol, bool ok) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+               "@p st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;\n\t}"
+               ::"l"(a), "f"((float)v), "l"(pol), "r"((int)ok) : "memory");
+}
+__device__ __forceinline__ void stp(double* a, double v, uint64_t pol, bool ok) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+               "@p st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;\n\t}"
+               ::"l"(a), "d"(v), "l"(pol), "r"((int)ok) : "memory");
+}
+__device__ __forceinline__ void stp(__nv_bfloat16* a, double v, uint64_t pol, bool ok) {
+  const __nv_bfloat16 b = __float2bfloat16_rn((float)v);
+  const unsigned short u = *reinterpret_cast<const unsigned short*>(&b);
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+               "@p st.global.L1::no_allocate.L2::cache_hint.u16 [%0], %1, %2;\n\t}"
+               ::"l"(a), "h"(u), "l"(pol), "r"((int)ok) : "memory");
+}
+
+// ---- mbarrier (CTA-local producer/consumer handoff of the per-warp partials)
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
+               ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n\t}"
+               ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
@@ -141,26 +204,95 @@ __device__ __forceinline__ void row_decode(const FPlan& P, int64_t rho, int64_t&
 }
 
 constexpr int kLag = 2;  // pass2 runs kLag iterations behind pass1
+constexpr int kU = 8;    // time steps per batch of predicated loads (memory-level parallelism)
+
+// CTA-local reduction of per-warp partials: every warp deposits NV values per
+// lane into a parity slot and arrives on full[par]; the NT reducer warps wait,
+// sum the warps that share their 32-column tile in fixed order, publish one
+// partial per (CTA, column) to global memory, release the group's grid
+// counter and free the slot (empty[par]).  No __syncthreads in the loop.
+struct CtaRed {
+  double* slot;      // [2][NW][NV][32]
+  uint64_t* full;    // [2]
+  uint64_t* empty;   // [2]
+};
+
+template <int NW, int NV>
+__device__ __forceinline__ void cta_deposit(const CtaRed& R, int g, int wl, int lane, const double (&val)[NV]) {
+  const int par = g & 1;
+  if (g >= 2) mbar_wait(R.empty + par, (unsigned)(((g - 2) >> 1) & 1));
+  double* sl = R.slot + ((size_t)(par * NW + wl) * NV) * 32 + lane;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) sl[v * 32] = val[v];
+  mbar_arrive(R.full + par);
+}
+
+// reducer warps only: returns after the partials of (CTA, group g) are in global
+// memory and the grid counter of group g has been released
+template <int NW, int NV>
+__device__ __forceinline__ void cta_reduce(const CtaRed& R, const FPlan& P, int g, int wl, int lane, int64_t c0,
+                                           int64_t ncols, double* part, unsigned* ctr) {
+  const int par = g & 1;
+  mbar_wait(R.full + par, (unsigned)((g >> 1) & 1));
+  const int64_t cg = (int64_t)wl * 32 + lane;
+  const bool ok = cg < ncols;
+  const int64_t plane = (int64_t)P.nCTA * P.J;
+  const int64_t o = (int64_t)blockIdx.x * P.J + c0 * P.Q + cg;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = 0.0;
+    for (int w2 = wl; w2 < NW; w2 += P.NT) a += R.slot[((size_t)(par * NW + w2) * NV + v) * 32 + lane];
+    if (ok) part[v * plane + o] = a;
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) red_release(ctr + 2 * g, 1u);
+  mbar_arrive(R.empty + par);
+}
+
+template <int NW, int NV>
+__device__ __forceinline__ CtaRed cta_red_setup(double* smem) {
+  CtaRed R;
+  R.slot = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)2 * NW * NV * 32);
+  R.full = bars;
+  R.empty = bars + 2;
+  return R;
+}
+
+template <int NW, int NV>
+constexpr size_t cta_red_smem_bytes() {
+  return sizeof(double) * 2 * NW * NV * 32 + 4 * sizeof(uint64_t);
+}
+
+template <int NW>
+__device__ __forceinline__ void cta_red_init(const CtaRed& R, int NT) {
+  if (threadIdx.x == 0) {
+    mbar_init(R.full + 0, NW * 32);
+    mbar_init(R.full + 1, NW * 32);
+    mbar_init(R.empty + 0, NT * 32);
+    mbar_init(R.empty + 1, NT * 32);
+  }
+  __syncthreads();
+}
 
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-template <int K, typename IO, int U>
+template <int K, typename IO>
 __device__ __forceinline__ void fwd_pass1_piece(const IO* __restrict__ base, int64_t step, int64_t s0, int64_t len,
                                                 bool cv, const double (&w)[K], double sh, double& S1, double& S2,
                                                 uint64_t pol) {
   double xw[K];
 #pragma unroll
-  for (int m = 1; m < K; ++m) {
-    const int64_t sp = s0 - K + m;
-    xw[m] = (cv && sp >= 0) ? ldhw(base + (int64_t)(m - K) * step, pol) : 0.0;
-  }
-  for (int64_t s = 0; s < len; s += U) {
-    double v[U];
+  for (int m = 1; m < K; ++m) xw[m] = ldpw(base + (int64_t)(m - K) * step, pol, cv && s0 - K + m >= 0);
+  for (int64_t s = 0; s < len; s += kU) {
+    double v[kU];
+    const IO* pb = base + s * step;
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = (cv && s + u < len) ? ldhw(base + (s + u) * step, pol) : 0.0;
+    for (int u = 0; u < kU; ++u) v[u] = ldpw(pb + u * step, pol, cv && s + u < len);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
       xw[K - 1] = v[u];
@@ -175,22 +307,21 @@ __device__ __forceinline__ void fwd_pass1_piece(const IO* __restrict__ base, int
   }
 }
 
-template <int K, typename IO, int U, int MODE, bool MULADD>
+template <int K, typename IO, int MODE, bool MULADD>
 __device__ __forceinline__ void fwd_pass2_piece(const IO* __restrict__ base, IO* __restrict__ obase, int64_t step,
                                                 int64_t s0, int64_t len, bool cv, const double (&wq)[K], double bf,
                                                 int skind, double alpha, uint64_t pol_in, uint64_t pol_out) {
   double xw[K];
 #pragma unroll
-  for (int m = 1; m < K; ++m) {
-    const int64_t sp = s0 - K + m;
-    xw[m] = (cv && sp >= 0) ? ldhw(base + (int64_t)(m - K) * step, pol_in) : 0.0;
-  }
-  for (int64_t s = 0; s < len; s += U) {
-    double v[U];
+  for (int m = 1; m < K; ++m) xw[m] = ldpw(base + (int64_t)(m - K) * step, pol_in, cv && s0 - K + m >= 0);
+  for (int64_t s = 0; s < len; s += kU) {
+    double v[kU];
+    const IO* pb = base + s * step;
+    IO* po = obase + s * step;
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = (cv && s + u < len) ? ldhw(base + (s + u) * step, pol_in) : 0.0;
+    for (int u = 0; u < kU; ++u) v[u] = ldpw(pb + u * step, pol_in, cv && s + u < len);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
       xw[K - 1] = v[u];
@@ -203,18 +334,16 @@ __device__ __forceinline__ void fwd_pass2_piece(const IO* __restrict__ base, IO*
         for (int i = 0; i < K; ++i) h = fma(wq[i], xw[i], h);
       }
       h = __dadd_rn(h, bf);
-      if (cv && s + u < len) {
-        double o;
-        if (MODE == 1) {
-          const double h2 = std::is_same<IO, double>::value ? h : round_f32(h);
-          o = surrogate_primitive(skind, alpha, h2);
-        } else if (std::is_same<IO, double>::value) {
-          o = h >= 0.0 ? 1.0 : 0.0;
-        } else {
-          o = h >= -0x1p-150 ? 1.0 : 0.0;  // == (f32(h) >= 0)
-        }
-        sth(obase + (s + u) * step, o, pol_out);
+      double o;
+      if (MODE == 1) {
+        const double h2 = std::is_same<IO, double>::value ? h : round_f32(h);
+        o = surrogate_primitive(skind, alpha, h2);
+      } else if (std::is_same<IO, double>::value) {
+        o = h >= 0.0 ? 1.0 : 0.0;
+      } else {
+        o = h >= -0x1p-150 ? 1.0 : 0.0;  // == (f32(h) >= 0)
       }
+      stp(po + u * step, o, pol_out, cv && s + u < len);
     }
   }
 }
@@ -293,12 +422,21 @@ __device__ void fwd_fold_channel(const FPlan& P, int64_t c, const double* __rest
   __threadfence();
 }
 
+// group bounds
+__device__ __forceinline__ void group_cols(const FPlan& P, int g, int64_t& c0, int64_t& c1) {
+  c0 = (int64_t)g * P.cpg;
+  c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+}
+
 template <int K, typename IO, int NW, int MODE, bool MULADD>
 __global__ void __launch_bounds__(NW * 32, 1)
     fused_fwd_kernel(FPlan P, const IO* __restrict__ x, const double* __restrict__ W, const double* gamma,
                      const double* beta, double* rm, double* rv, int flags, double eps, double momentum, int skind,
                      double alpha, IO* __restrict__ out, double* fold, double* part, unsigned* ctr) {
-  constexpr int U = 8;
+  constexpr int NV = 2;
+  extern __shared__ __align__(16) double smem_f[];
+  const CtaRed R = cta_red_setup<NW, NV>(smem_f);
+  cta_red_init<NW>(R, P.NT);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wg = blockIdx.x * NW + wl;
   const int tile = wg % P.NT;
@@ -308,93 +446,74 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int64_t rho1 = active ? (int64_t)(slice + 1) * P.R / P.S : 0;
   const bool shared = flags & PSN_SHARED;
   const int64_t step = (int64_t)P.d * P.row;
-  const int64_t plane = (int64_t)P.nCTA * P.J;
-  __shared__ double sred[2][NW][32];
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
   const int iters = P.G + kLag;
   for (int it = 0; it < iters; ++it) {
     // ---------------- pass 1 of group `it`: shifted moments of h1 ----------
     if (it < P.G) {
       const int g = it;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int64_t colg = (int64_t)tile * 32 + lane;
       const bool cv = active && colg < (c1 - c0) * P.Q;
-      const int64_t col = c0 * P.Q + colg;
-      const int64_t c = cv ? col / P.Q : c0;
+      const int64_t col = c0 * P.Q + (cv ? colg : 0);
+      const int64_t c = col / P.Q;
       double w[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) w[i] = cv ? __ldg(W + (shared ? 0 : c * K) + i) : 0.0;
-      const double sh = cv ? __ldcg(rm + c) : 0.0;
-      double S1 = 0.0, S2 = 0.0;
+      for (int i = 0; i < K; ++i) w[i] = __ldg(W + (shared ? 0 : c * K) + i);
+      const double sh = __ldcg(rm + c);
+      double acc[NV] = {0.0, 0.0};
       for (int64_t rho = rho0; rho < rho1;) {
         int64_t n, s, Sr;
         int r;
         row_decode(P, rho, n, r, s, Sr);
         const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
         const IO* base = x + (r + s * P.d) * P.row + n * P.J + col;
-        fwd_pass1_piece<K, IO, U>(base, step, s, len, cv, w, sh, S1, S2, pol_keep);
+        fwd_pass1_piece<K, IO>(base, step, s, len, cv, w, sh, acc[0], acc[1], pol_keep);
         rho += len;
       }
-      sred[0][wl][lane] = S1;
-      sred[1][wl][lane] = S2;
-      __syncthreads();
-      if (wl < P.NT) {
-        double a1 = 0.0, a2 = 0.0;
-        for (int w2 = wl; w2 < NW; w2 += P.NT) {
-          a1 += sred[0][w2][lane];
-          a2 += sred[1][w2][lane];
-        }
-        const int64_t cg2 = (int64_t)wl * 32 + lane;
-        if (cg2 < (c1 - c0) * P.Q) {
-          const int64_t o = (int64_t)blockIdx.x * P.J + c0 * P.Q + cg2;
-          part[o] = a1;
-          part[plane + o] = a2;
-        }
-        __threadfence();
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) red_release(ctr + 2 * g, 1u);
+      cta_deposit<NW, NV>(R, g, wl, lane, acc);
+      if (wl < P.NT) cta_reduce<NW, NV>(R, P, g, wl, lane, c0, (c1 - c0) * P.Q, part, ctr);
     }
     // ---------------- fold of group it-1 (one warp per channel) -----------
     if (it >= 1 && it - 1 < P.G) {
       const int g = it - 1;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int rot = (int)(((int64_t)g * 37) % P.nCTA);
       const int first = ((int)blockIdx.x - rot + P.nCTA) % P.nCTA;
       int li = 0;
       for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
         if ((li % NW) != wl) continue;
-        wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
+        wait_geq(ctr + 2 * g, (unsigned)(P.nCTA * P.NT));
         fwd_fold_channel(P, c, part, W, flags, gamma, beta, rm, rv, eps, momentum, fold, lane);
         __syncwarp();
         if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
       }
     }
     // ---------------- pass 2 of group it-kLag: spikes ----------------------
-    if (it >= kLag && it - kLag < P.G) {
+    if (it >= kLag && it - kLag < P.G && active) {
       const int g = it - kLag;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int64_t colg = (int64_t)tile * 32 + lane;
-      const bool cv = active && colg < (c1 - c0) * P.Q;
-      const int64_t col = c0 * P.Q + colg;
-      const int64_t c = cv ? col / P.Q : c0;
-      if (active) wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      const bool cv = colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + (cv ? colg : 0);
+      const int64_t c = col / P.Q;
+      wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
       double wq[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) wq[i] = cv ? __ldcg(f + PSN_FOLD_HDR + K + i) : 0.0;
-      const double bf = cv ? __ldcg(f + 3) : 0.0;
+      for (int i = 0; i < K; ++i) wq[i] = __ldcg(f + PSN_FOLD_HDR + K + i);
+      const double bf = __ldcg(f + 3);
       for (int64_t rho = rho0; rho < rho1;) {
         int64_t n, s, Sr;
         int r;
         row_decode(P, rho, n, r, s, Sr);
         const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
         const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
-        fwd_pass2_piece<K, IO, U, MODE, MULADD>(x + off, out + off, step, s, len, cv, wq, bf, skind, alpha,
-                                                pol_drop, pol_drop);
+        fwd_pass2_piece<K, IO, MODE, MULADD>(x + off, out + off, step, s, len, cv, wq, bf, skind, alpha, pol_drop,
+                                             pol_drop);
         rho += len;
       }
     }
@@ -405,11 +524,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
 // backward
 // partials: [NV][nCTA][J] with NV = 3K+1: db, dwq[K], sx[K], sxc[K]
 // ---------------------------------------------------------------------------
-template <int K>
-struct BwdAcc {
-  double db, dwq[K], sxa, sxc[K], tail[K];
-};
-
 // f64 surrogate derivative (reference surrogate.py:36-38) on the f32-rounded h2
 struct SurD {
   int kind;
@@ -437,32 +551,33 @@ __device__ __forceinline__ double surrogate_grad_f64(const SurD& sd, double h) {
 // the per-channel sums db, dw_q are f64 — per-element f32 errors would grow
 // ~sqrt(m) in these m-term reductions.  The BN-term sums (sx, sxc) only reach
 // dW through the 1/m-scaled alpha1/beta1 and use f32 within a batch.
-template <int K, typename IO, int U>
+template <int K, typename IO>
 __device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const IO* __restrict__ yb, int64_t step,
                                                 int64_t s0, int64_t len, int64_t Sr, bool cv, const float (&w)[K],
                                                 const double (&wqd)[K], double bfd, float mu, const SurD& sd,
-                                                BwdAcc<K>& A, uint64_t pol) {
+                                                double (&acc)[3 * K + 1], double (&tail)[K], uint64_t pol) {
   float xw[K];
   double xwd[K];
 #pragma unroll
   for (int m = 1; m < K; ++m) {
-    const int64_t sp = s0 - K + m;
-    xw[m] = (cv && sp >= 0) ? ldh(xb + (int64_t)(m - K) * step, pol) : 0.0f;
+    xw[m] = ldp(xb + (int64_t)(m - K) * step, pol, cv && s0 - K + m >= 0);
     xwd[m] = (double)xw[m];
   }
-  for (int64_t s = 0; s < len; s += U) {
-    float xv[U], yv[U];
+  for (int64_t s = 0; s < len; s += kU) {
+    float xv[kU], yv[kU];
+    const IO* px = xb + s * step;
+    const IO* py = yb + s * step;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const bool ok = cv && s + u < len;
-      xv[u] = ok ? ldh(xb + (s + u) * step, pol) : 0.0f;
-      yv[u] = ok ? ldh(yb + (s + u) * step, pol) : 0.0f;
+      xv[u] = ldp(px + u * step, pol, ok);
+      yv[u] = ldp(py + u * step, pol, ok);
     }
     float fsa = 0.0f, fsc[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) fsc[i] = 0.0f;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) {
         xw[i] = xw[i + 1];
@@ -477,9 +592,9 @@ __device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const
       const double h2 = std::is_same<IO, double>::value ? h : round_f32(h);
       const bool ok = s + u < len;
       const double dh2 = ok ? (double)yv[u] * surrogate_grad_f64(sd, h2) : 0.0;
-      A.db += dh2;
+      acc[0] += dh2;
 #pragma unroll
-      for (int i = 0; i < K; ++i) A.dwq[i] = fma(xwd[i], dh2, A.dwq[i]);
+      for (int i = 0; i < K; ++i) acc[1 + i] = fma(xwd[i], dh2, acc[1 + i]);
       float h1 = 0.0f;
 #pragma unroll
       for (int i = 0; i < K; ++i) h1 = fmaf(w[i], xw[i], h1);
@@ -488,25 +603,26 @@ __device__ __forceinline__ void bwd_passA_piece(const IO* __restrict__ xb, const
 #pragma unroll
       for (int i = 0; i < K; ++i) fsc[i] = fmaf(xw[i], hc, fsc[i]);
     }
-    A.sxa += (double)fsa;
 #pragma unroll
-    for (int i = 0; i < K; ++i) A.sxc[i] += (double)fsc[i];
+    for (int i = 0; i < K; ++i) {
+      acc[1 + K + i] += (double)fsa;  // Sx: all x, minus the stream tails below
+      acc[1 + 2 * K + i] += (double)fsc[i];
+    }
   }
   // Sx[i] = sum over t of x[t - off_i] excludes the last K-1-i steps of the stream
   if (s0 + len == Sr && cv) {
 #pragma unroll
     for (int dist = 0; dist < K - 1; ++dist) {
       const int64_t p = len - 1 - dist;  // relative step, may precede this piece
-      if (s0 + p < 0) continue;
-      const float xv = ldh(xb + p * step, pol);
+      const float xv = ldp(xb + p * step, pol, s0 + p >= 0);
 #pragma unroll
       for (int i = 0; i < K - 1; ++i)
-        if (i < K - 1 - dist) A.tail[i] += (double)xv;
+        if (i < K - 1 - dist) tail[i] += (double)xv;
     }
   }
 }
 
-template <int K, typename IO, int U>
+template <int K, typename IO>
 __device__ __forceinline__ void bwd_passB_piece(const IO* __restrict__ xb, const IO* __restrict__ yb,
                                                 IO* __restrict__ ob, int64_t step, int64_t s0, int64_t len,
                                                 int64_t Sr, bool cv, const float (&w)[K], const float (&wq)[K],
@@ -514,23 +630,23 @@ __device__ __forceinline__ void bwd_passB_piece(const IO* __restrict__ xb, const
                                                 uint64_t pol_in, uint64_t pol_out) {
   float xw[K], pacc[K];
 #pragma unroll
-  for (int m = 1; m < K; ++m) {
-    const int64_t sp = s0 - K + m;
-    xw[m] = (cv && sp >= 0) ? ldh(xb + (int64_t)(m - K) * step, pol_in) : 0.0f;
-  }
+  for (int m = 1; m < K; ++m) xw[m] = ldp(xb + (int64_t)(m - K) * step, pol_in, cv && s0 - K + m >= 0);
 #pragma unroll
   for (int i = 0; i < K; ++i) pacc[i] = 0.0f;
   const int64_t nsteps = len + K - 1;  // dh needed on [s0, s0+len+K-1) within the stream
-  for (int64_t s = 0; s < nsteps; s += U) {
-    float xv[U], yv[U];
+  for (int64_t s = 0; s < nsteps; s += kU) {
+    float xv[kU], yv[kU];
+    const IO* px = xb + s * step;
+    const IO* py = yb + s * step;
+    IO* po = ob + (s - (K - 1)) * step;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const bool ok = cv && s + u < nsteps && s0 + s + u < Sr;
-      xv[u] = ok ? ldh(xb + (s + u) * step, pol_in) : 0.0f;
-      yv[u] = ok ? ldh(yb + (s + u) * step, pol_in) : 0.0f;
+      xv[u] = ldp(px + u * step, pol_in, ok);
+      yv[u] = ldp(py + u * step, pol_in, ok);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kU; ++u) {
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
       xw[K - 1] = xv[u];
@@ -550,7 +666,7 @@ __device__ __forceinline__ void bwd_passB_piece(const IO* __restrict__ xb, const
         pacc[i] = fmaf(w[i], dh1, pacc[i]);
       }
       const int64_t o = s + u - (K - 1);
-      if (cv && o >= 0 && o < len) sth(ob + o * step, (double)pacc[0], pol_out);
+      stp(po + u * step, (double)pacc[0], pol_out, cv && o >= 0 && o < len);
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) pacc[i] = pacc[i + 1];
       pacc[K - 1] = 0.0f;
@@ -627,10 +743,12 @@ template <int K, typename IO, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     fused_bwd_kernel(FPlan P, const IO* __restrict__ x, const IO* __restrict__ dy, const double* __restrict__ W,
                      const double* gamma, const double* fold, int flags, Surrogate sur, SurD sd,
-                     IO* __restrict__ dx,
-                     double* dW, double* dgamma, double* dbeta, double* bfold, double* part, unsigned* ctr) {
-  constexpr int U = 8;
-  const int NV = 3 * K + 1;
+                     IO* __restrict__ dx, double* dW, double* dgamma, double* dbeta, double* bfold, double* part,
+                     unsigned* ctr) {
+  constexpr int NV = 3 * K + 1;
+  extern __shared__ __align__(16) double smem_b[];
+  const CtaRed R = cta_red_setup<NW, NV>(smem_b);
+  cta_red_init<NW>(R, P.NT);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wg = blockIdx.x * NW + wl;
   const int tile = wg % P.NT;
@@ -640,129 +758,99 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int64_t rho1 = active ? (int64_t)(slice + 1) * P.R / P.S : 0;
   const bool shared = flags & PSN_SHARED;
   const int64_t step = (int64_t)P.d * P.row;
-  const int64_t plane = (int64_t)P.nCTA * P.J;
-  __shared__ double sred[4][NW][32];
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
   const int iters = P.G + kLag;
   for (int it = 0; it < iters; ++it) {
     // ---------------- pass A of group `it`: per-column sums ----------------
     if (it < P.G) {
       const int g = it;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int64_t colg = (int64_t)tile * 32 + lane;
       const bool cv = active && colg < (c1 - c0) * P.Q;
-      const int64_t col = c0 * P.Q + colg;
-      const int64_t c = cv ? col / P.Q : c0;
+      const int64_t col = c0 * P.Q + (cv ? colg : 0);
+      const int64_t c = col / P.Q;
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
       float w[K];
       double wqd[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        w[i] = cv ? (float)__ldg(W + (shared ? 0 : c * K) + i) : 0.0f;
-        wqd[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;
+        w[i] = (float)__ldg(W + (shared ? 0 : c * K) + i);
+        wqd[i] = __ldg(f + PSN_FOLD_HDR + K + i);
       }
-      const double bfd = cv ? __ldg(f + 3) : 0.0;
-      const float mu = cv ? (float)__ldg(f + 0) : 0.0f;
-      BwdAcc<K> A;
-      A.db = A.sxa = 0.0;
+      const double bfd = __ldg(f + 3);
+      const float mu = (float)__ldg(f + 0);
+      double acc[NV], tail[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) A.dwq[i] = A.sxc[i] = A.tail[i] = 0.0;
+      for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) tail[i] = 0.0;
       for (int64_t rho = rho0; rho < rho1;) {
         int64_t n, s, Sr;
         int r;
         row_decode(P, rho, n, r, s, Sr);
         const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
         const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
-        bwd_passA_piece<K, IO, U>(x + off, dy + off, step, s, len, Sr, cv, w, wqd, bfd, mu, sd, A, pol_keep);
+        bwd_passA_piece<K, IO>(x + off, dy + off, step, s, len, Sr, cv, w, wqd, bfd, mu, sd, acc, tail, pol_keep);
         rho += len;
       }
-      // CTA reduction, 4 values per round, then one partial per (CTA, column)
-      for (int v0 = 0; v0 < NV; v0 += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int v = v0 + u;
-          double val = 0.0;
-          if (v == 0) val = A.db;
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            if (v == 1 + i) val = A.dwq[i];
-            if (v == 1 + K + i) val = A.sxa - (i < K - 1 ? A.tail[i] : 0.0);
-            if (v == 1 + 2 * K + i) val = A.sxc[i];
-          }
-          sred[u][wl][lane] = val;
-        }
-        __syncthreads();
-        if (wl < P.NT) {
-          const int64_t cg2 = (int64_t)wl * 32 + lane;
-          const bool ok = cg2 < (c1 - c0) * P.Q;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int v = v0 + u;
-            if (v < NV) {
-              double a = 0.0;
-              for (int w2 = wl; w2 < NW; w2 += P.NT) a += sred[u][w2][lane];
-              if (ok) part[v * plane + (int64_t)blockIdx.x * P.J + c0 * P.Q + cg2] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-      if (wl < P.NT) __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) red_release(ctr + 2 * g, 1u);
+      for (int i = 0; i < K - 1; ++i) acc[1 + K + i] -= tail[i];
+      cta_deposit<NW, NV>(R, g, wl, lane, acc);
+      if (wl < P.NT) cta_reduce<NW, NV>(R, P, g, wl, lane, c0, (c1 - c0) * P.Q, part, ctr);
     }
     // ---------------- fold of group it-1 ------------------------------------
     if (it >= 1 && it - 1 < P.G) {
       const int g = it - 1;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int rot = (int)(((int64_t)g * 37) % P.nCTA);
       const int first = ((int)blockIdx.x - rot + P.nCTA) % P.nCTA;
       int li = 0;
       for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
         if ((li % NW) != wl) continue;
-        wait_geq(ctr + 2 * g, (unsigned)P.nCTA);
+        wait_geq(ctr + 2 * g, (unsigned)(P.nCTA * P.NT));
         bwd_fold_channel(P, c, part, W, flags, gamma, fold, dW, dgamma, dbeta, bfold, lane);
         __syncwarp();
         if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
       }
     }
     // ---------------- pass B of group it-kLag: dx --------------------------
-    if (it >= kLag && it - kLag < P.G) {
+    if (it >= kLag && it - kLag < P.G && active) {
       const int g = it - kLag;
-      const int64_t c0 = (int64_t)g * P.cpg;
-      const int64_t c1 = (c0 + P.cpg < P.C) ? c0 + P.cpg : P.C;
+      int64_t c0, c1;
+      group_cols(P, g, c0, c1);
       const int64_t colg = (int64_t)tile * 32 + lane;
-      const bool cv = active && colg < (c1 - c0) * P.Q;
-      const int64_t col = c0 * P.Q + colg;
-      const int64_t c = cv ? col / P.Q : c0;
-      if (active) wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      const bool cv = colg < (c1 - c0) * P.Q;
+      const int64_t col = c0 * P.Q + (cv ? colg : 0);
+      const int64_t c = col / P.Q;
+      wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
       float w[K], wq[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        w[i] = cv ? (float)__ldg(W + (shared ? 0 : c * K) + i) : 0.0f;
-        wq[i] = cv ? (float)__ldg(f + PSN_FOLD_HDR + K + i) : 0.0f;
+        w[i] = (float)__ldg(W + (shared ? 0 : c * K) + i);
+        wq[i] = (float)__ldg(f + PSN_FOLD_HDR + K + i);
       }
-      const float bf = cv ? (float)__ldg(f + 3) : 0.0f;
-      const float mu = cv ? (float)__ldg(f + 0) : 0.0f;
-      const float a1 = cv ? (float)__ldcg(bfold + 2 * c) : 0.0f;
-      const float b1 = cv ? (float)__ldcg(bfold + 2 * c + 1) : 0.0f;
+      const float bf = (float)__ldg(f + 3);
+      const float mu = (float)__ldg(f + 0);
+      const float a1 = (float)__ldcg(bfold + 2 * c);
+      const float b1 = (float)__ldcg(bfold + 2 * c + 1);
       for (int64_t rho = rho0; rho < rho1;) {
         int64_t n, s, Sr;
         int r;
         row_decode(P, rho, n, r, s, Sr);
         const int64_t len = (rho1 - rho < Sr - s) ? rho1 - rho : Sr - s;
         const int64_t off = (r + s * P.d) * P.row + n * P.J + col;
-        bwd_passB_piece<K, IO, U>(x + off, dy + off, dx + off, step, s, len, Sr, cv, w, wq, bf, mu, a1, b1, sur,
-                                  pol_drop, pol_drop);
+        bwd_passB_piece<K, IO>(x + off, dy + off, dx + off, step, s, len, Sr, cv, w, wq, bf, mu, a1, b1, sur,
+                               pol_drop, pol_drop);
         rho += len;
       }
     }
   }
 }
 
+// ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -853,9 +941,9 @@ static FusedWs carve(void* ws, const FPlan& P) {
 
 // co-resident CTAs of a kernel instance (cooperative launch needs all of them)
 template <typename F>
-static int resident_ctas(F kernel, int block) {
+static int resident_ctas(F kernel, int block, size_t smem) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel, block, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kernel, block, smem) != cudaSuccess) {
     (void)cudaGetLastError();
     return 0;
   }
@@ -869,10 +957,15 @@ static void fit_grid(FPlan& P, int resident) {
 }
 
 template <typename F>
-static int coop_launch(F kernel, FPlan& P, int block, void** args, cudaStream_t st) {
-  fit_grid(P, resident_ctas(kernel, block));
+static int coop_launch(F kernel, FPlan& P, int block, size_t smem, void** args, cudaStream_t st) {
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(PSN_ERR_CUDA, "cannot raise the dynamic shared memory limit of the fused kernel");
+  }
+  fit_grid(P, resident_ctas(kernel, block, smem));
   const int grid = P.nCTA;
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, 0, st);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(block), args, smem, st);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return fail(PSN_ERR_CUDA, cudaGetErrorString(e));
@@ -897,11 +990,11 @@ int fused_forward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, con
   const bool smooth = flags & PSN_SMOOTH;
   const bool muladd = !((flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH)));
   if (smooth) {
-    if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, true>, P, kFwdNW * 32, args, st);
-    return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, false>, P, kFwdNW * 32, args, st);
+    if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, true>, P, kFwdNW * 32, cta_red_smem_bytes<kFwdNW, 2>(), args, st);
+    return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 1, false>, P, kFwdNW * 32, cta_red_smem_bytes<kFwdNW, 2>(), args, st);
   }
-  if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, true>, P, kFwdNW * 32, args, st);
-  return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, false>, P, kFwdNW * 32, args, st);
+  if (muladd) return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, true>, P, kFwdNW * 32, cta_red_smem_bytes<kFwdNW, 2>(), args, st);
+  return coop_launch(fused_fwd_kernel<K, IO, kFwdNW, 0, false>, P, kFwdNW * 32, cta_red_smem_bytes<kFwdNW, 2>(), args, st);
 }
 
 template <int K, typename IO>
@@ -938,7 +1031,7 @@ int fused_backward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, co
   double* dWp = shared ? dwtmp : dW;
   void* args[] = {&P, &xp, &yp, (void*)&W, (void*)&gamma, (void*)&fold, &flags, &sur, &sd, &op, &dWp, &dgamma,
                   &dbeta, &w.bfold, &w.part, &w.ctr};
-  return coop_launch(fused_bwd_kernel<K, IO, kBwdNW>, P, kBwdNW * 32, args, st);
+  return coop_launch(fused_bwd_kernel<K, IO, kBwdNW>, P, kBwdNW * 32, cta_red_smem_bytes<kBwdNW, 3 * K + 1>(), args, st);
 }
 
 #define PSN_FK_CASES(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
