@@ -168,6 +168,37 @@ __device__ __forceinline__ void wait_geq(const unsigned* a, unsigned target) {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
+// CTA-cooperative wait on a grid counter: at most one warp of the CTA polls
+// global memory at a time (a brief try-lock, never held while sleeping), and
+// every observed event is cached in a shared-memory ring so the other warps of
+// the CTA see it without touching L2.  Keeps the number of pollers of a
+// counter at <= #CTAs instead of #warps.
+struct CtaSync {
+  unsigned* ring;  // [64] observed event keys
+  unsigned* lock;  // [1]
+};
+__device__ __forceinline__ void cta_wait(const CtaSync& S, const unsigned* gctr, unsigned target, unsigned key,
+                                         int lane) {
+  volatile unsigned* slot = S.ring + (key & 63u);
+  if (lane == 0) {
+    while (*slot < key) {  // keys sharing a slot only grow
+      if (atomicCAS(S.lock, 0u, 1u) == 0u) {
+        if (*slot < key && ld_relaxed(gctr) >= target) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          *slot = key;
+        }
+        atomicExch(S.lock, 0u);
+      }
+      if (*slot < key) __nanosleep(128);
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// grid counters live on separate 128-byte lines
+__device__ __forceinline__ unsigned* ctr_b1(unsigned* ctr, int g) { return ctr + (size_t)(2 * g) * 32; }
+__device__ __forceinline__ unsigned* ctr_b2(unsigned* ctr, int g) { return ctr + (size_t)(2 * g + 1) * 32; }
+
 // f32 rounding of an f64 value with two DADDs (exact (double)(float)h for every
 // |h| below FLT_MAX, denormals included): adding M = 1.5 * 2^(E+29) moves the
 // rounding point of the sum to 2^(E-23) = ulp_f32(h), ties-to-even preserved.
@@ -246,7 +277,7 @@ __device__ __forceinline__ void cta_reduce(const CtaRed& R, const FPlan& P, int 
   }
   __threadfence();
   __syncwarp();
-  if (lane == 0) red_release(ctr + 2 * g, 1u);
+  if (lane == 0) red_release(ctr_b1(ctr, g), 1u);
   mbar_arrive(R.empty + par);
 }
 
@@ -262,11 +293,20 @@ __device__ __forceinline__ CtaRed cta_red_setup(double* smem) {
 
 template <int NW, int NV>
 constexpr size_t cta_red_smem_bytes() {
-  return sizeof(double) * 2 * NW * NV * 32 + 4 * sizeof(uint64_t);
+  return sizeof(double) * 2 * NW * NV * 32 + 4 * sizeof(uint64_t) + 65 * sizeof(unsigned);
+}
+
+template <int NW, int NV>
+__device__ __forceinline__ CtaSync cta_sync_setup(double* smem) {
+  CtaSync S;
+  S.ring = reinterpret_cast<unsigned*>(reinterpret_cast<uint64_t*>(smem + (size_t)2 * NW * NV * 32) + 4);
+  S.lock = S.ring + 64;
+  return S;
 }
 
 template <int NW>
-__device__ __forceinline__ void cta_red_init(const CtaRed& R, int NT) {
+__device__ __forceinline__ void cta_red_init(const CtaRed& R, const CtaSync& S, int NT) {
+  for (int i = threadIdx.x; i < 65; i += blockDim.x) S.ring[i] = 0u;
   if (threadIdx.x == 0) {
     mbar_init(R.full + 0, NW * 32);
     mbar_init(R.full + 1, NW * 32);
@@ -436,7 +476,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int NV = 2;
   extern __shared__ __align__(16) double smem_f[];
   const CtaRed R = cta_red_setup<NW, NV>(smem_f);
-  cta_red_init<NW>(R, P.NT);
+  const CtaSync S = cta_sync_setup<NW, NV>(smem_f);
+  cta_red_init<NW>(R, S, P.NT);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wg = blockIdx.x * NW + wl;
   const int tile = wg % P.NT;
@@ -485,10 +526,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
       int li = 0;
       for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
         if ((li % NW) != wl) continue;
-        wait_geq(ctr + 2 * g, (unsigned)(P.nCTA * P.NT));
+        cta_wait(S, ctr_b1(ctr, g), (unsigned)(P.nCTA * P.NT), 2u * g + 1u, lane);
         fwd_fold_channel(P, c, part, W, flags, gamma, beta, rm, rv, eps, momentum, fold, lane);
         __syncwarp();
-        if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
+        if (lane == 0) red_release(ctr_b2(ctr, g), 1u);
       }
     }
     // ---------------- pass 2 of group it-kLag: spikes ----------------------
@@ -500,7 +541,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const bool cv = colg < (c1 - c0) * P.Q;
       const int64_t col = c0 * P.Q + (cv ? colg : 0);
       const int64_t c = col / P.Q;
-      wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      cta_wait(S, ctr_b2(ctr, g), (unsigned)(c1 - c0), 2u * g + 2u, lane);
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
       double wq[K];
 #pragma unroll
@@ -748,7 +789,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int NV = 3 * K + 1;
   extern __shared__ __align__(16) double smem_b[];
   const CtaRed R = cta_red_setup<NW, NV>(smem_b);
-  cta_red_init<NW>(R, P.NT);
+  const CtaSync S = cta_sync_setup<NW, NV>(smem_b);
+  cta_red_init<NW>(R, S, P.NT);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int wg = blockIdx.x * NW + wl;
   const int tile = wg % P.NT;
@@ -809,10 +851,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
       int li = 0;
       for (int64_t c = c0 + first; c < c1; c += P.nCTA, ++li) {
         if ((li % NW) != wl) continue;
-        wait_geq(ctr + 2 * g, (unsigned)(P.nCTA * P.NT));
+        cta_wait(S, ctr_b1(ctr, g), (unsigned)(P.nCTA * P.NT), 2u * g + 1u, lane);
         bwd_fold_channel(P, c, part, W, flags, gamma, fold, dW, dgamma, dbeta, bfold, lane);
         __syncwarp();
-        if (lane == 0) red_release(ctr + 2 * g + 1, 1u);
+        if (lane == 0) red_release(ctr_b2(ctr, g), 1u);
       }
     }
     // ---------------- pass B of group it-kLag: dx --------------------------
@@ -824,7 +866,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const bool cv = colg < (c1 - c0) * P.Q;
       const int64_t col = c0 * P.Q + (cv ? colg : 0);
       const int64_t c = col / P.Q;
-      wait_geq(ctr + 2 * g + 1, (unsigned)(c1 - c0));
+      cta_wait(S, ctr_b2(ctr, g), (unsigned)(c1 - c0), 2u * g + 2u, lane);
       const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
       float w[K], wq[K];
 #pragma unroll
@@ -916,7 +958,7 @@ size_t fused_workspace_bytes(const psn_desc_t* desc) {
     FPlan P;
     if (!fused_plan(desc, b == 1, P)) continue;
     const size_t nv = b ? 3 * (size_t)P.k + 1 : 2;
-    size_t bytes = 256 + 8 * (2 * (size_t)P.G) + 8 * nv * (size_t)P.nCTA * P.J + 16 * (size_t)P.C + 1024;
+    size_t bytes = 256 + 128 * (2 * (size_t)P.G) + 8 * nv * (size_t)P.nCTA * P.J + 16 * (size_t)P.C + 1024;
     if (bytes > need) need = bytes;
   }
   return need;
@@ -932,7 +974,7 @@ static FusedWs carve(void* ws, const FPlan& P) {
   FusedWs w;
   char* p = (char*)ws;
   w.ctr = (unsigned*)p;
-  size_t off = ((size_t)2 * P.G * sizeof(unsigned) + 255) & ~(size_t)255;
+  size_t off = ((size_t)2 * P.G * 128 + 255) & ~(size_t)255;
   w.bfold = (double*)(p + off);
   off += ((size_t)16 * P.C + 255) & ~(size_t)255;
   w.part = (double*)(p + off);
@@ -978,7 +1020,7 @@ int fused_forward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, con
                     const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
   FPlan P = Pin;
   FusedWs w = carve(ws, P);
-  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * P.G, st) != cudaSuccess)
+  if (cudaMemsetAsync(w.ctr, 0, (size_t)2 * 128 * P.G, st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of fused counters failed");
   int flags = desc->flags;
   double eps = desc->eps, mom = desc->momentum, alpha = desc->alpha;
@@ -1003,7 +1045,7 @@ int fused_backward_k(const psn_desc_t* desc, const FPlan& Pin, const void* x, co
                      double* dwtmp, void* ws, cudaStream_t st) {
   FPlan P = Pin;
   FusedWs w = carve(ws, P);
-  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * P.G, st) != cudaSuccess)
+  if (cudaMemsetAsync(w.ctr, 0, (size_t)2 * 128 * P.G, st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of fused counters failed");
   int flags = desc->flags;
   const bool shared = flags & PSN_SHARED;
