@@ -129,6 +129,22 @@ __device__ __forceinline__ void stp(__nv_bfloat16* a, double v, uint64_t pol, bo
                ::"l"(a), "h"(u), "l"(pol), "r"((int)ok) : "memory");
 }
 
+// ---- watchdog: a wait that exceeds PSN_WAIT_LIMIT_NS reports itself and traps,
+// so a scheduling bug surfaces as a CUDA error instead of a hung device
+#ifndef PSN_WAIT_LIMIT_NS
+#define PSN_WAIT_LIMIT_NS 4000000000ull
+#endif
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void wait_expired(const char* what, unsigned a, unsigned b) {
+  printf("psn fused kernel: wait '%s' expired (block %d warp %d, %u/%u)\n", what, (int)blockIdx.x,
+         (int)(threadIdx.x >> 5), a, b);
+  __trap();
+}
+
 // ---- mbarrier (CTA-local producer/consumer handoff of the per-warp partials)
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
@@ -138,11 +154,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
                ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
 }
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n\t.reg .pred p;\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+               "selp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(ok) : "r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-               "@!p bra WAIT_%=;\n\t}"
-               ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+  if (mbar_try_wait(b, parity)) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (!mbar_try_wait(b, parity)) {
+    if (globaltimer_ns() - t0 > PSN_WAIT_LIMIT_NS) wait_expired("mbarrier", parity, 0);
+  }
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
@@ -181,7 +206,9 @@ __device__ __forceinline__ void cta_wait(const CtaSync& S, const unsigned* gctr,
                                          int lane) {
   volatile unsigned* slot = S.ring + (key & 63u);
   if (lane == 0) {
+    const unsigned long long t0 = globaltimer_ns();
     while (*slot < key) {  // keys sharing a slot only grow
+      if (globaltimer_ns() - t0 > PSN_WAIT_LIMIT_NS) wait_expired("grid counter", key, target);
       if (atomicCAS(S.lock, 0u, 1u) == 0u) {
         if (*slot < key && ld_relaxed(gctr) >= target) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
