@@ -24,6 +24,7 @@
 // spikes equal the reference's whenever (w_q, b_f) do; the Heaviside compares
 // h2 against -2^-150, which is exactly "f32(h2) >= 0".  Backward arithmetic is
 // f32 (FFMA) with f64 accumulation of the per-channel sums every U steps.
+#include <stdio.h>
 #include <string.h>
 
 #include <mutex>
@@ -132,7 +133,7 @@ __device__ __forceinline__ void stp(__nv_bfloat16* a, double v, uint64_t pol, bo
 // ---- watchdog: a wait that exceeds PSN_WAIT_LIMIT_NS reports itself and traps,
 // so a scheduling bug surfaces as a CUDA error instead of a hung device
 #ifndef PSN_WAIT_LIMIT_NS
-#define PSN_WAIT_LIMIT_NS 4000000000ull
+#define PSN_WAIT_LIMIT_NS 2000000000ull
 #endif
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
