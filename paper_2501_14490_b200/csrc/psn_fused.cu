@@ -194,30 +194,35 @@ __device__ __forceinline__ void wait_geq(const unsigned* a, unsigned target) {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-// CTA-cooperative wait on a grid counter: at most one warp of the CTA polls
-// global memory at a time (a brief try-lock, never held while sleeping), and
-// every observed event is cached in a shared-memory ring so the other warps of
-// the CTA see it without touching L2.  Keeps the number of pollers of a
-// counter at <= #CTAs instead of #warps.
+// CTA-cooperative wait on a grid counter.  Observed events are cached in a
+// shared-memory ring (slot = key & 63, keys sharing a slot only grow), and the
+// global counter of an event is polled at most once per ~0.5 us per CTA: a
+// waiter claims the poll by CAS-ing the slot's timestamp, so no lock is ever
+// held across the (slow) global load and no waiter can starve another event's
+// waiter.  Keeps L2 traffic on a counter at <= #CTAs polls per 0.5 us.
 struct CtaSync {
-  unsigned* ring;  // [64] observed event keys
-  unsigned* lock;  // [1]
+  unsigned* ring;   // [64] observed event keys
+  unsigned* stamp;  // [64] last poll time per slot (globaltimer >> 5)
 };
 __device__ __forceinline__ void cta_wait(const CtaSync& S, const unsigned* gctr, unsigned target, unsigned key,
                                          int lane) {
   volatile unsigned* slot = S.ring + (key & 63u);
-  if (lane == 0) {
+  unsigned* stamp = S.stamp + (key & 63u);
+  if (lane == 0 && *slot < key) {
     const unsigned long long t0 = globaltimer_ns();
-    while (*slot < key) {  // keys sharing a slot only grow
-      if (globaltimer_ns() - t0 > PSN_WAIT_LIMIT_NS) wait_expired("grid counter", key, target);
-      if (atomicCAS(S.lock, 0u, 1u) == 0u) {
-        if (*slot < key && ld_relaxed(gctr) >= target) {
+    while (*slot < key) {
+      const unsigned long long tn = globaltimer_ns();
+      const unsigned now = (unsigned)(tn >> 5);
+      const unsigned last = *(volatile unsigned*)stamp;
+      if (now - last >= 16u && atomicCAS(stamp, last, now) == last) {
+        if (ld_relaxed(gctr) >= target) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          *slot = key;
+          atomicMax((unsigned*)slot, key);
         }
-        atomicExch(S.lock, 0u);
+      } else {
+        __nanosleep(200);
       }
-      if (*slot < key) __nanosleep(128);
+      if (tn - t0 > PSN_WAIT_LIMIT_NS) wait_expired("grid counter", key, target);
     }
   }
   __syncwarp();
@@ -321,20 +326,20 @@ __device__ __forceinline__ CtaRed cta_red_setup(double* smem) {
 
 template <int NW, int NV>
 constexpr size_t cta_red_smem_bytes() {
-  return sizeof(double) * 2 * NW * NV * 32 + 4 * sizeof(uint64_t) + 65 * sizeof(unsigned);
+  return sizeof(double) * 2 * NW * NV * 32 + 4 * sizeof(uint64_t) + 128 * sizeof(unsigned);
 }
 
 template <int NW, int NV>
 __device__ __forceinline__ CtaSync cta_sync_setup(double* smem) {
   CtaSync S;
   S.ring = reinterpret_cast<unsigned*>(reinterpret_cast<uint64_t*>(smem + (size_t)2 * NW * NV * 32) + 4);
-  S.lock = S.ring + 64;
+  S.stamp = S.ring + 64;
   return S;
 }
 
 template <int NW>
 __device__ __forceinline__ void cta_red_init(const CtaRed& R, const CtaSync& S, int NT) {
-  for (int i = threadIdx.x; i < 65; i += blockDim.x) S.ring[i] = 0u;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) S.ring[i] = 0u;  // ring + stamps
   if (threadIdx.x == 0) {
     mbar_init(R.full + 0, NW * 32);
     mbar_init(R.full + 1, NW * 32);
