@@ -162,26 +162,6 @@ __device__ __forceinline__ double surrogate_primitive(int kind, double alpha, do
   return atan(r * h) / r + 0.5;
 }
 
-// ---- fused (persistent) path plan, psn_fused.cu -------------------------------
-struct FPlan {
-  int64_t T, N, C, Q, J, row, R;  // R = N*T rows of (n, residue, step)
-  int d, k;
-  int q, m;        // T = q*d + m: residues r < m have q+1 steps, the rest q
-  int nCTA, NW;    // grid and warps per CTA
-  int NT;          // 32-column tiles per group (power of two dividing NW)
-  int64_t cpg;     // channels per group
-  int G;           // groups
-  int S;           // row slices per tile
-};
-
-bool fused_plan(const psn_desc_t* desc, bool backward, FPlan& P);
-size_t fused_workspace_bytes(const psn_desc_t* desc);
-int fused_forward(const psn_desc_t* desc, const FPlan& P, const void* x, const double* W, const double* gamma,
-                  const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st);
-int fused_backward(const psn_desc_t* desc, const FPlan& P, const void* x, const void* dy, const double* W,
-                   const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
-                   double* dwtmp, void* ws, cudaStream_t st);
-
 // ---- host-side helpers shared by the translation units (psn_layer.cu) ----------
 int fail(int code, const char* msg);
 int cuda_check(const char* where);

@@ -21,6 +21,7 @@
 #include <type_traits>
 
 #include "psn_common.cuh"
+#include "psn_stream_dispatch.h"
 
 namespace psn {
 
@@ -96,7 +97,7 @@ WsLayout ws_layout(const psn_desc_t* desc) {
   w.evalfold = off;
   off = align256(off + sizeof(double) * (PSN_FOLD_HDR + 2 * (size_t)g.k) * g.C);
   w.fused = off;
-  off = align256(off + fused_workspace_bytes(desc));
+  off = align256(off + stream::workspace_bytes(desc));
   w.total = off;
   return w;
 }
@@ -796,11 +797,11 @@ int psn_forward_train(const psn_desc_t* desc, const void* x, const double* W, co
     return rc;
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
-  FPlan P;
-  if (fused_plan(desc, false, P)) {
-    rc = fused_forward(desc, P, x, W, gamma, beta, running_mean, running_var, out, fold,
-                       (char*)workspace + L.fused, (cudaStream_t)stream);
-    return rc ? rc : cuda_check("psn_forward_train (fused)");
+  stream::Plan P;
+  if (stream::make_plan(desc, false, P)) {
+    rc = stream::forward(desc, P, x, W, gamma, beta, running_mean, running_var, out, fold,
+                         (char*)workspace + L.fused, (cudaStream_t)stream);
+    return rc ? rc : cuda_check("psn_forward_train (stream)");
   }
   return by_dtype_k<FwdOp>(desc, desc, g, x, W, gamma, beta, running_mean, running_var, out, fold,
                            (char*)workspace, L, (cudaStream_t)stream);
@@ -819,14 +820,15 @@ int psn_backward(const psn_desc_t* desc, const void* x, const void* dy, const do
     return rc;
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
-  FPlan P;
-  if (fused_plan(desc, true, P)) {
+  stream::Plan P;
+  if (stream::make_plan(desc, true, P)) {
     double* dwtmp = (double*)((char*)workspace + L.dwtmp);
-    rc = fused_backward(desc, P, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, dwtmp,
-                        (char*)workspace + L.fused, (cudaStream_t)stream);
+    const bool shared = desc->flags & PSN_SHARED;
+    rc = stream::backward(desc, P, x, dy, W, gamma, fold, dx, shared ? dwtmp : dW, dgamma, dbeta,
+                          (char*)workspace + L.fused, (cudaStream_t)stream);
     if (rc) return rc;
-    if (desc->flags & PSN_SHARED) shared_rowsum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dwtmp, desc->C, desc->k, dW);
-    return cuda_check("psn_backward (fused)");
+    if (shared) shared_rowsum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dwtmp, desc->C, desc->k, dW);
+    return cuda_check("psn_backward (stream)");
   }
   return by_dtype_k<BwdOp>(desc, desc, g, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, (char*)workspace, L,
                            (cudaStream_t)stream);
@@ -847,6 +849,29 @@ int psn_forward_eval(const psn_desc_t* desc, const void* x, const double* W, con
   double* fold = (double*)((char*)workspace + ws_layout(desc).evalfold);
   return by_dtype_k<EvalOp>(desc, desc, g, x, W, gamma, beta, running_mean, running_var, out, fold,
                             (cudaStream_t)stream);
+}
+
+// Execution plan of psn_forward_train (backward = 0) / psn_backward (1):
+// info = {streamed (1) or generic (0), CTAs, groups, tiles per group, stages,
+//         kernel launches per call (memsets included)}.
+int psn_plan_info(const psn_desc_t* desc, int backward, int64_t* info, int n) {
+  if (!desc || !info || n <= 0 || validate(desc, false) != PSN_OK) return 0;
+  int64_t v[6] = {0, 0, 0, 0, 0, 3};
+  const int rowsum = (backward && (desc->flags & PSN_SHARED)) ? 1 : 0;
+  stream::Plan P;
+  if (stream::make_plan(desc, backward != 0, P)) {
+    v[0] = 1;
+    v[1] = P.nCTA;
+    v[2] = P.G;
+    v[3] = P.tpg;
+    v[4] = P.S;
+    v[5] = 2 + rowsum;
+  } else {
+    v[5] = 3 + rowsum;
+  }
+  const int m = n < 6 ? n : 6;
+  for (int i = 0; i < m; ++i) info[i] = v[i];
+  return m;
 }
 
 }  // extern "C"

@@ -1,0 +1,228 @@
+// psn_stream.cu — host side of the TMA-staged persistent PSN kernels
+// (psn_stream.cuh): eligibility, planning, workspace, tensor-map encoding and
+// the (order, dilation, carrier) dispatch.
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "psn_stream.cuh"
+#include "psn_stream_dispatch.h"
+
+namespace psn {
+namespace stream {
+
+static int g_sms = 0, g_smem_optin = 0;
+static std::once_flag g_dev_once;
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static void dev_init() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  cudaGetLastError();
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static int tb_for(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
+
+int stage_bytes_for(int k, int d, int es, bool bwd) {
+  const int H = (k - 1) * d;
+  const int TB = tb_for(es, bwd);
+  const int xrows = TB > H ? TB : H;
+  const int rowb = kConsumerWarps * kCols * es;
+  const int xb = xrows * rowb, db = bwd ? xrows * rowb : 0;
+  const int pst = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
+  return ((xb + db + kCols * pst) + 1023) / 1024 * 1024;
+}
+
+bool eligible(const psn_desc_t* desc) {
+  if (env_int("PSN_FORCE_GENERIC", 0)) return false;
+  if (desc->dtype != PSN_F32 && desc->dtype != PSN_BF16) return false;
+  if (desc->Q != 1) return false;                 // spatial inputs: generic path
+  if (desc->k > 8 || desc->d > 3) return false;   // instantiated orders / sawtooth dilations
+  if ((desc->k - 1) * desc->d > kMaxH) return false;
+  if (desc->flags & PSN_SMOOTH) return false;     // SMOOTH (finite-difference checks): generic path
+  const int es = (int)dtype_size(desc->dtype);
+  if ((desc->C * es) % 16 != 0) return false;     // TMA row stride must be a multiple of 16 B
+  if (desc->T > (1 << 30) || desc->N > (1 << 30) || desc->C > (1 << 30)) return false;
+  return true;
+}
+
+bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
+  if (!eligible(desc)) return false;
+  std::call_once(g_dev_once, dev_init);
+  if (!g_encode || g_sms <= 0) return false;
+  const int es = (int)dtype_size(desc->dtype);
+  p.T = (int)desc->T;
+  p.N = (int)desc->N;
+  p.C = (int)desc->C;
+  p.J = p.C;
+  p.k = desc->k;
+  p.d = desc->d;
+  p.H = (p.k - 1) * p.d;
+  p.TB = tb_for(es, bwd);
+  p.G = (p.C + kCols - 1) / kCols;
+  p.nbk = (p.N + kConsumerWarps - 1) / kConsumerWarps;
+  p.ttl = (p.T + p.TB - 1) / p.TB;
+  const long long tpg = (long long)p.nbk * p.ttl;
+  if (tpg > (1 << 30)) return false;
+  p.tpg = (int)tpg;
+  p.nCTA = g_sms;
+  p.P = p.tpg < p.nCTA ? p.tpg : p.nCTA;
+  if (p.P > 160) return false;  // fold reads at most 5 slots per lane
+  int F = bwd ? env_int("PSN_FOLD_BWD", 8) : env_int("PSN_FOLD_FWD", 2);
+  if (F != 1 && F != 2 && F != 4 && F != 8 && F != 16 && F != 32) F = bwd ? 8 : 2;
+  while (F > p.nCTA) F >>= 1;
+  p.F = F;
+  p.lag = env_int("PSN_LAG", 2);
+  if (p.lag < 1) p.lag = 1;
+  p.stage_bytes = stage_bytes_for(p.k, p.d, es, bwd);
+  const int budget = (g_smem_optin > 0 ? g_smem_optin : 232448) - kRedBytes - 2048;
+  int S = budget / p.stage_bytes;
+  const int smax = env_int("PSN_STAGES", 8);
+  if (S > smax) S = smax;
+  if (S < 2) return false;
+  p.S = S;
+  return true;
+}
+
+static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// workspace: counters | bfold | partials
+size_t workspace_bytes(const psn_desc_t* desc) {
+  size_t need = 0;
+  for (int b = 0; b < 2; ++b) {
+    Plan p;
+    if (!make_plan(desc, b == 1, p)) continue;
+    const size_t nv = b ? 3 * (size_t)p.k + 1 : 2;
+    const size_t bytes = a256(2 * sizeof(unsigned) * p.G) + a256(2 * sizeof(double) * p.C) +
+                         a256(sizeof(double) * p.G * nv * kCols * p.P);
+    if (bytes > need) need = bytes;
+  }
+  return need;
+}
+
+int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const void* dy, CUtensorMap* maps) {
+  memset(maps, 0, 4 * sizeof(CUtensorMap));
+  const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const cuuint64_t dims[3] = {(cuuint64_t)p.J, (cuuint64_t)p.N, (cuuint64_t)p.T};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.J * es, (cuuint64_t)p.J * p.N * es};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapL2promotion prom = es == 4 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  for (int m = 0; m < 4; ++m) {
+    const bool is_dy = m >= 2, halo = m & 1;
+    if (is_dy && !bwd) continue;
+    if (halo && p.H == 0) continue;
+    const cuuint32_t box[3] = {(cuuint32_t)kCols, (cuuint32_t)kConsumerWarps, (cuuint32_t)(halo ? p.H : p.TB)};
+    CUresult r = g_encode(&maps[m], dt, 3, const_cast<void*>(is_dy ? dy : x), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PSN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  return PSN_OK;
+}
+
+struct Ws {
+  unsigned* ctr;
+  double* bfold;
+  double* part;
+};
+
+static Ws carve(void* ws, const Plan& p) {
+  Ws w;
+  char* b = (char*)ws;
+  w.ctr = (unsigned*)b;
+  b += a256(2 * sizeof(unsigned) * p.G);
+  w.bfold = (double*)b;
+  b += a256(2 * sizeof(double) * p.C);
+  w.part = (double*)b;
+  return w;
+}
+
+static int dispatch(const psn_desc_t* desc, bool bwd, const Args& a, const void* x, const void* dy, cudaStream_t st) {
+  const int k = desc->k, d = desc->d;
+  if (desc->dtype == PSN_F32)
+    return bwd ? run_f32_bwd(k, d, a, x, dy, st) : run_f32_fwd(k, d, a, x, dy, st);
+  return bwd ? run_bf16_bwd(k, d, a, x, dy, st) : run_bf16_fwd(k, d, a, x, dy, st);
+}
+
+int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* W, const double* gamma,
+            const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
+  Ws w = carve(ws, p);
+  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * p.G, st) != cudaSuccess)
+    return fail(PSN_ERR_CUDA, "memset of stream counters failed");
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.p = p;
+  a.out = out;
+  a.W = W;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.rm = rm;
+  a.rv = rv;
+  a.fold = fold;
+  a.bfold = w.bfold;
+  a.part = w.part;
+  a.cnt = w.ctr;
+  a.fdone = w.ctr + p.G;
+  a.flags = desc->flags;
+  a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
+  a.eps = desc->eps;
+  a.momentum = desc->momentum;
+  return dispatch(desc, false, a, x, nullptr, st);
+}
+
+int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* dy, const double* W,
+             const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
+             void* ws, cudaStream_t st) {
+  Ws w = carve(ws, p);
+  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * p.G, st) != cudaSuccess)
+    return fail(PSN_ERR_CUDA, "memset of stream counters failed");
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.p = p;
+  a.out = dx;
+  a.W = W;
+  a.gamma = gamma;
+  a.fold = const_cast<double*>(fold);
+  a.dW = dW;
+  a.dgamma = dgamma;
+  a.dbeta = dbeta;
+  a.bfold = w.bfold;
+  a.part = w.part;
+  a.cnt = w.ctr;
+  a.fdone = w.ctr + p.G;
+  a.flags = desc->flags;
+  a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
+  a.eps = desc->eps;
+  a.momentum = desc->momentum;
+  Surrogate s;
+  s.kind = desc->surrogate;
+  if (desc->surrogate == PSN_ARCTAN) {
+    s.c = (float)(0.5 * 3.141592653589793 * desc->alpha);
+    s.scale = (float)(desc->alpha / 2.0);
+  } else {
+    s.c = (float)desc->alpha;
+    s.scale = 1.0f;
+  }
+  a.sur = s;
+  a.skind = desc->surrogate;
+  a.sc = desc->surrogate == PSN_ARCTAN ? 0.5 * 3.141592653589793 * desc->alpha : desc->alpha;
+  a.sscale = desc->surrogate == PSN_ARCTAN ? desc->alpha / 2.0 : 1.0;
+  return dispatch(desc, true, a, x, dy, st);
+}
+
+}  // namespace stream
+}  // namespace psn
