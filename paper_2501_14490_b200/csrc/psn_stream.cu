@@ -35,18 +35,6 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-static int tb_for(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
-
-int stage_bytes_for(int k, int d, int es, bool bwd) {
-  const int H = (k - 1) * d;
-  const int TB = tb_for(es, bwd);
-  const int xrows = TB > H ? TB : H;
-  const int rowb = kConsumerWarps * kCols * es;
-  const int xb = xrows * rowb, db = bwd ? xrows * rowb : 0;
-  const int pst = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
-  return ((xb + db + kCols * pst) + 1023) / 1024 * 1024;
-}
-
 bool eligible(const psn_desc_t* desc) {
   if (env_int("PSN_FORCE_GENERIC", 0)) return false;
   if (desc->dtype != PSN_F32 && desc->dtype != PSN_BF16) return false;
@@ -72,7 +60,8 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   p.k = desc->k;
   p.d = desc->d;
   p.H = (p.k - 1) * p.d;
-  p.TB = tb_for(es, bwd);
+  const Layout L = layout_of(p.k, p.d, es, bwd);
+  p.TB = L.TB;
   p.G = (p.C + kCols - 1) / kCols;
   p.nbk = (p.N + kConsumerWarps - 1) / kConsumerWarps;
   p.ttl = (p.T + p.TB - 1) / p.TB;
@@ -81,15 +70,11 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   p.tpg = (int)tpg;
   p.nCTA = g_sms;
   p.P = p.tpg < p.nCTA ? p.tpg : p.nCTA;
-  if (p.P > 160) return false;  // fold reads at most 5 slots per lane
-  int F = bwd ? env_int("PSN_FOLD_BWD", 8) : env_int("PSN_FOLD_FWD", 2);
-  if (F != 1 && F != 2 && F != 4 && F != 8 && F != 16 && F != 32) F = bwd ? 8 : 2;
-  while (F > p.nCTA) F >>= 1;
-  p.F = F;
   p.lag = env_int("PSN_LAG", 2);
-  if (p.lag < 1) p.lag = 1;
-  p.stage_bytes = stage_bytes_for(p.k, p.d, es, bwd);
-  const int budget = (g_smem_optin > 0 ? g_smem_optin : 232448) - kRedBytes - 2048;
+  if (p.lag < 2) p.lag = 2;  // the publisher stages pass-2 parameters one iteration ahead
+  if (p.lag > 6) p.lag = 6;  // its ring of pre-update running statistics holds 8 groups
+  p.stage_bytes = L.stage;
+  const int budget = (g_smem_optin > 0 ? g_smem_optin : 232448) - L.fixed - 2048;
   int S = budget / p.stage_bytes;
   const int smax = env_int("PSN_STAGES", 8);
   if (S > smax) S = smax;
@@ -100,15 +85,18 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-// workspace: counters | bfold | partials
+// workspace: group counters | per-channel f64 sums (both zeroed per launch)
+static size_t zeroed_bytes(const Plan& p, bool bwd) {
+  const size_t nv = bwd ? 3 * (size_t)p.k + 1 : 2;
+  return a256(sizeof(unsigned) * p.G) + sizeof(double) * p.G * nv * kCols;
+}
+
 size_t workspace_bytes(const psn_desc_t* desc) {
   size_t need = 0;
   for (int b = 0; b < 2; ++b) {
     Plan p;
     if (!make_plan(desc, b == 1, p)) continue;
-    const size_t nv = b ? 3 * (size_t)p.k + 1 : 2;
-    const size_t bytes = a256(2 * sizeof(unsigned) * p.G) + a256(2 * sizeof(double) * p.C) +
-                         a256(sizeof(double) * p.G * nv * kCols * p.P);
+    const size_t bytes = a256(zeroed_bytes(p, b == 1));
     if (bytes > need) need = bytes;
   }
   return need;
@@ -135,19 +123,14 @@ int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const voi
 }
 
 struct Ws {
-  unsigned* ctr;
-  double* bfold;
-  double* part;
+  unsigned* cnt;
+  double* acc;
 };
 
 static Ws carve(void* ws, const Plan& p) {
   Ws w;
-  char* b = (char*)ws;
-  w.ctr = (unsigned*)b;
-  b += a256(2 * sizeof(unsigned) * p.G);
-  w.bfold = (double*)b;
-  b += a256(2 * sizeof(double) * p.C);
-  w.part = (double*)b;
+  w.cnt = (unsigned*)ws;
+  w.acc = (double*)((char*)ws + a256(sizeof(unsigned) * p.G));
   return w;
 }
 
@@ -161,7 +144,7 @@ static int dispatch(const psn_desc_t* desc, bool bwd, const Args& a, const void*
 int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* W, const double* gamma,
             const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
   Ws w = carve(ws, p);
-  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * p.G, st) != cudaSuccess)
+  if (cudaMemsetAsync(ws, 0, zeroed_bytes(p, false), st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of stream counters failed");
   Args a;
   memset(&a, 0, sizeof(a));
@@ -173,14 +156,14 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
   a.rm = rm;
   a.rv = rv;
   a.fold = fold;
-  a.bfold = w.bfold;
-  a.part = w.part;
-  a.cnt = w.ctr;
-  a.fdone = w.ctr + p.G;
+  a.cnt = w.cnt;
+  a.acc = w.acc;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;
   a.momentum = desc->momentum;
+  a.trace = env_int("PSN_TRACE", 0);
+  a.dbg = env_int("PSN_DBG", 0);
   return dispatch(desc, false, a, x, nullptr, st);
 }
 
@@ -188,7 +171,7 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
              const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
              void* ws, cudaStream_t st) {
   Ws w = carve(ws, p);
-  if (cudaMemsetAsync(w.ctr, 0, 2 * sizeof(unsigned) * p.G, st) != cudaSuccess)
+  if (cudaMemsetAsync(ws, 0, zeroed_bytes(p, true), st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of stream counters failed");
   Args a;
   memset(&a, 0, sizeof(a));
@@ -200,14 +183,14 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
   a.dW = dW;
   a.dgamma = dgamma;
   a.dbeta = dbeta;
-  a.bfold = w.bfold;
-  a.part = w.part;
-  a.cnt = w.ctr;
-  a.fdone = w.ctr + p.G;
+  a.cnt = w.cnt;
+  a.acc = w.acc;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;
   a.momentum = desc->momentum;
+  a.trace = env_int("PSN_TRACE", 0);
+  a.dbg = env_int("PSN_DBG", 0);
   Surrogate s;
   s.kind = desc->surrogate;
   if (desc->surrogate == PSN_ARCTAN) {

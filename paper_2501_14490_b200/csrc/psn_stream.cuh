@@ -47,10 +47,10 @@ namespace psn {
 namespace stream {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + TMA producer warp + publisher warp
 constexpr int kCols = 32;                        // columns per tile (lanes)
-constexpr int kRedBytes = 8 * kConsumerWarps * 32 * (int)sizeof(double);  // 16 KB
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
+constexpr int kRowBlock = 8;                     // time rows a consumer thread advances at once (ILP)
 
 #ifndef PSN_WAIT_LIMIT_NS
 #define PSN_WAIT_LIMIT_NS 4000000000ull
@@ -68,7 +68,6 @@ struct Plan {
   int ttl;         // ceil(T / TB)
   int tpg;         // tiles per group = nbk * ttl
   int P;           // workers per (pass, group) = min(nCTA, tpg)
-  int F;           // folder CTAs per group
   int nCTA;
   int lag;         // pass2 runs `lag` iterations behind pass1 (>= 1)
   int S;           // pipeline stages
@@ -87,14 +86,14 @@ struct Args {
   double* dW;             // [C,k] (or per-channel scratch when shared)
   double* dgamma;
   double* dbeta;
-  double* bfold;          // [C][2] backward BN-through-stats scalars (alpha1, beta1)
-  double* part;           // [G][NV][32][P] per-CTA partial sums
-  unsigned* cnt;          // [G] pass-1 arrivals
-  unsigned* fdone;        // [G] folder completions
+  double* acc;            // [G][NV][32] per-channel pass-1 sums (f64 atomic adds, zeroed per launch)
+  unsigned* cnt;          // [G] pass-1 arrivals (every CTA arrives once per group)
   int flags;
   int shared;
   double eps, momentum;
   Surrogate sur;    // f32 surrogate (dx pass)
+  int dbg;           // PSN_DBG ablation mask (benchmarking only): 1 skip stores, 2 skip pass-1 math, 4 skip pass-2 math
+  int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
   double sc, sscale; // f64 surrogate: arctan c = pi*alpha/2, scale = alpha/2; rational c = alpha, scale = 1
   int skind;
 };
@@ -202,8 +201,28 @@ __device__ __forceinline__ void st_out(__nv_bfloat16* a, float v, uint64_t pol) 
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(a), "h"(u), "l"(pol) : "memory");
 }
 
-__device__ __forceinline__ float lds(const float* p) { return *p; }
-__device__ __forceinline__ float lds(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+// explicit shared-space loads (the stage pointers are computed from an aligned
+// integer, so the compiler would otherwise emit generic LD for them)
+__device__ __forceinline__ float lds(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(su32(p)));
+  return v;
+}
+__device__ __forceinline__ float lds(const __nv_bfloat16* p) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(su32(p)));
+  return __uint_as_float(((unsigned)v) << 16);
+}
+__device__ __forceinline__ double ldsd(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(su32(p)));
+  return v;
+}
+__device__ __forceinline__ float ldsf(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(su32(p)));
+  return v;
+}
 
 // exact (double)(float)h with two DADDs (F2F.F32.F64 issues at ~8/clk/SM on
 // B200, DADD at 64): adding M = 1.5 * 2^(E+29) puts the rounding point of the
@@ -224,23 +243,40 @@ __device__ __forceinline__ double rcp_f64(double v) {
 }
 
 // -------------------------------------------------------------------------
-// configuration per (order, dilation, carrier, direction)
+// shared-memory layout per (order, dilation, carrier size, direction); host
+// planning (stage count) and the kernel both use it
 // -------------------------------------------------------------------------
+struct Layout {
+  int H, NV, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
+};
+__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
+__host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
+  Layout L{};
+  L.H = (k - 1) * d;
+  L.NV = bwd ? 3 * k + 1 : 2;
+  L.TB = tile_rows(es, bwd);
+  L.rowb = kConsumerWarps * kCols * es;  // bytes of one time row of a box
+  const int xrows = L.TB > L.H ? L.TB : L.H;
+  L.xbytes = xrows * L.rowb;
+  L.dbytes = bwd ? xrows * L.rowb : 0;
+  // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
+  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
+  L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
+  L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
+  L.dep = kConsumerWarps * L.NV * kCols * 8;  // per-warp partial sums handed to the publisher
+  L.tot = 8 * 2 * kCols * 8;                  // publisher ring: pre-update running stats of 8 groups
+  L.fixed = L.dep + 4 * L.pbytes + L.tot + 512;
+  return L;
+}
+
 template <int K, int D, typename IO, bool BWD>
 struct Cfg {
-  static constexpr int H = (K - 1) * D;
-  static constexpr int NV = BWD ? 3 * K + 1 : 2;
-  static constexpr int ES = (int)sizeof(IO);
-  static constexpr int TB = BWD ? (ES == 4 ? 16 : 32) : (ES == 4 ? 32 : 64);
-  static constexpr int XROWS = TB > H ? TB : H;
-  static constexpr int ROWB = kConsumerWarps * kCols * ES;  // bytes of one time row of a box
-  static constexpr int XBYTES = XROWS * ROWB;
-  static constexpr int DBYTES = BWD ? XROWS * ROWB : 0;
-  // per-lane parameter bytes: fwd f64 {w or w_q}[K] + {shift or b_f}; bwd f64 w_q[K], b_f + f32 W[K], mu, a1, b1
-  static constexpr int PSTRIDE = BWD ? (8 * (K + 1) + 4 * (K + 3) + 15) / 16 * 16 : 8 * (K + 1);
-  static constexpr int PBYTES = kCols * PSTRIDE;
-  static constexpr int STAGE = ((XBYTES + DBYTES + PBYTES) + 1023) / 1024 * 1024;
+  static constexpr Layout L = layout_of(K, D, (int)sizeof(IO), BWD);
+  static constexpr int H = L.H, NV = L.NV, TB = L.TB;
+  static constexpr int XBYTES = L.xbytes, PSTRIDE = L.pstride, PBYTES = L.pbytes, STAGE = L.stage;
+  static constexpr int ROWB = L.rowb;
   static_assert(H <= kMaxH, "window above the streamed-path limit");
+  static_assert(TB % kRowBlock == 0, "tile rows must be a multiple of the row block");
 };
 
 // tap i reads x[t - (K-1-i)*D] = window slot H - (K-1-i)*D
@@ -250,20 +286,137 @@ __device__ __forceinline__ constexpr int slot(int i) {
 }
 
 // -------------------------------------------------------------------------
-// static schedule, shared by the producer and the consumers
+// static schedule, shared by the three warp roles
 // -------------------------------------------------------------------------
 __device__ __forceinline__ int worker_of(const Plan& p, int g, int pass) {
   const int rot = (int)(((long long)g * 61 + pass * 29) % p.nCTA);
   return ((int)blockIdx.x - rot + p.nCTA) % p.nCTA;
 }
-__device__ __forceinline__ int folder_of(const Plan& p, int g, int f) {
-  return (int)(((long long)g * p.F + f) % p.nCTA);
+__device__ __forceinline__ void tile_range(const Plan& p, int v, int& ta, int& tb) {
+  ta = (int)((long long)v * p.tpg / p.P);
+  tb = (int)((long long)(v + 1) * p.tpg / p.P);
 }
 
 enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
 
 // -------------------------------------------------------------------------
-// the kernel
+// fold of channel c from its per-channel pass-1 sums, one publisher lane per
+// channel (forward: network.py:239-258; backward: network.py:279-317).  Every
+// CTA folds the 32 channels of the group it is about to stream in pass 2 and
+// writes the pass-2 parameters straight into its shared-memory slot; only the
+// group's designated CTA (`store`) writes the layer outputs to global memory.
+// -------------------------------------------------------------------------
+template <int K, bool BWD>
+__device__ __forceinline__ void fold_channel(const Args& a, int c, const double* tt, double rm_prev, double rv_prev,
+                                             bool store, unsigned char* prow) {
+  const Plan& p = a.p;
+  const double* Wc = a.W + (a.shared ? 0 : (size_t)c * K);
+  double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
+  double* pd = (double*)prow;
+  const int flags = a.flags;
+  const double m = (double)p.T * (double)p.N;
+  if constexpr (!BWD) {
+    const bool smooth = flags & PSN_SMOOTH;
+    const bool use_batch = flags & PSN_USE_BATCH_STATS;
+    const bool quantize = (flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH));
+    const double dmean = tt[0] / m;
+    const double mu_b = rm_prev + dmean;  // the pass-1 shift was running_mean (pre-update)
+    double var_b = tt[1] / m - dmean * dmean;
+    var_b = var_b < 0.0 ? 0.0 : var_b;
+    const double mu = use_batch ? mu_b : rm_prev;  // network.py:250-255
+    const double var = use_batch ? var_b : rv_prev;
+    const double s = sqrt(var + a.eps);
+    const double aa = __ldg(a.gamma + c) / s;
+    const double bf = __ldg(a.beta + c) - aa * mu;
+    if (store) {
+      if (!smooth) {  // network.py:241-248
+        const double unbiased = m > 1.0 ? var_b * (m / (m - 1.0)) : var_b;
+        double r1 = rm_prev * (1.0 - a.momentum);
+        r1 = r1 + a.momentum * mu_b;
+        double r2 = rv_prev * (1.0 - a.momentum);
+        r2 = r2 + a.momentum * unbiased;
+        a.rm[c] = r1;
+        a.rv[c] = r2;
+      }
+      fr[0] = mu;
+      fr[1] = s;
+      fr[2] = aa;
+      fr[3] = bf;
+      fr[4] = mu_b;
+      fr[5] = var_b;
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const double wf = aa * __ldg(Wc + i);
+      double wq = wf;
+      if (quantize) {  // quant.py:111-139
+        int sg, e;
+        quantize_pow2(wf, sg, e);
+        wq = ldexp((double)sg, e);
+      }
+      if (store) {
+        fr[PSN_FOLD_HDR + i] = wf;
+        fr[PSN_FOLD_HDR + K + i] = wq;
+      }
+      pd[i] = wq;
+    }
+    pd[K] = bf;
+  } else {
+    float* pf = (float*)(prow + 8 * (K + 1));
+    const double mu = __ldg(fr + 0), s = __ldg(fr + 1), aa = __ldg(fr + 2);
+    const bool quantized = (flags & PSN_QUANTIZED) && (!(flags & PSN_SMOOTH) || (flags & PSN_QUANTIZE_IN_SMOOTH));
+    const double db_f = tt[0] * a.sscale;
+    double da = 0.0, dwf[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {  // quantize_backward, quant.py:194-216
+      double g1 = tt[1 + i] * a.sscale;
+      if (quantized && (flags & PSN_ROUND_STE)) {
+        const double wf = __ldg(fr + PSN_FOLD_HDR + i), wq = __ldg(fr + PSN_FOLD_HDR + K + i);
+        g1 = (wf != 0.0) ? g1 * (fabs(wq) / fabs(wf)) : 0.0;
+      }
+      dwf[i] = g1;
+      da = da + dwf[i] * __ldg(Wc + i);
+    }
+    da = da - db_f * mu;  // network.py:291-296
+    double alpha1 = 0.0, beta1 = 0.0;
+    if (flags & PSN_USE_BATCH_STATS) {  // network.py:298-315
+      const double ds = -da * __ldg(a.gamma + c) / (s * s);
+      const double dvar = ds / (2.0 * s);
+      const double dmu = -db_f * aa;
+      alpha1 = dmu / m;
+      beta1 = (2.0 / m) * dvar;
+    }
+    if (store) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double dw = aa * dwf[i];
+        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * tt[1 + K + i] + beta1 * tt[1 + 2 * K + i];
+        a.dW[(size_t)c * K + i] = dw;
+      }
+      a.dbeta[c] = db_f;
+      a.dgamma[c] = da / s;
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      pd[i] = __ldg(fr + PSN_FOLD_HDR + K + i);  // w_q
+      pf[i] = (float)__ldg(Wc + i);
+    }
+    pd[K] = __ldg(fr + 3);  // b_f
+    pf[K] = (float)mu;
+    pf[K + 1] = (float)alpha1;
+    pf[K + 2] = (float)beta1;
+  }
+}
+
+__device__ __forceinline__ int designated_of(const Plan& p, int g) { return (int)(((long long)g * 37 + 11) % p.nCTA); }
+
+__device__ __forceinline__ void red_add_f64(double* a, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+
+// -------------------------------------------------------------------------
+// the kernel: warps 0..7 consume tiles, warp 8 issues TMA, warp 9 publishes
+// partial sums, folds, and stages per-segment parameters
 // -------------------------------------------------------------------------
 template <int K, int D, typename IO, bool BWD>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -271,18 +424,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
                       const Args a) {
   using C_ = Cfg<K, D, IO, BWD>;
+  constexpr Layout LY = C_::L;
   constexpr int H = C_::H, NV = C_::NV, TB = C_::TB;
   const Plan& p = a.p;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  double* red = (double*)(smem + (size_t)p.S * C_::STAGE);
-  uint64_t* full = (uint64_t*)(smem + (size_t)p.S * C_::STAGE + kRedBytes);
+  double* dep = (double*)(smem + (size_t)p.S * C_::STAGE);
+  unsigned char* p1s = (unsigned char*)dep + LY.dep;
+  unsigned char* p2s = p1s + 2 * LY.pbytes;
+  double* tot = (double*)(p2s + 2 * LY.pbytes);
+  uint64_t* full = (uint64_t*)((unsigned char*)tot + LY.tot);
   uint64_t* empty = full + p.S;
+  uint64_t* depf = empty + p.S;
+  uint64_t* depe = depf + 1;
+  uint64_t* p1f = depe + 1;
+  uint64_t* p1e = p1f + 2;
+  uint64_t* p2f = p1e + 2;
+  uint64_t* p2e = p2f + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsumerWarps);
+    }
+    mbar_init(depf, kConsumerWarps);
+    mbar_init(depe, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(p1f + i, 1);
+      mbar_init(p1e + i, kConsumerWarps);
+      mbar_init(p2f + i, 1);
+      mbar_init(p2e + i, kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -291,57 +462,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int iters = p.G + p.lag;
 
   if (warp == kConsumerWarps) {
-    // ======================= producer warp =======================
+    // ======================= producer warp: TMA only =======================
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mx) : "memory");
       if (H > 0) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mxh) : "memory");
       if (BWD) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&my) : "memory");
       if (BWD && H > 0) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&myh) : "memory");
-    }
-    const uint64_t pol_keep = pol_evict_last(), pol_drop = pol_evict_first(), pol_norm = pol_evict_normal();
-    int q = 0;
-    auto issue = [&](int kind, int pass, int g, int nbi, int trow, bool params) {
-      const int s = q % p.S;
-      if (q >= p.S) {
-        if (lane == 0) mbar_wait(empty + s, (unsigned)(((q / p.S) - 1) & 1));
-        __syncwarp();
-      }
-      unsigned char* st = smem + (size_t)s * C_::STAGE;
-      if (params) {
-        // per-channel parameters of this segment, one lane per column
-        const int c = g * kCols + lane;
-        const bool cv = c < p.C;
-        const int cc = cv ? c : 0;
-        const int wr = a.shared ? 0 : cc;
-        unsigned char* pr = st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE;
-        const double* f = a.fold + (size_t)cc * (PSN_FOLD_HDR + 2 * K);
-        if (!BWD) {
-          double* pd = (double*)pr;
-          if (pass == 0) {
-#pragma unroll
-            for (int i = 0; i < K; ++i) pd[i] = cv ? __ldg(a.W + (size_t)wr * K + i) : 0.0;
-            pd[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments
-          } else {
-#pragma unroll
-            for (int i = 0; i < K; ++i) pd[i] = cv ? __ldcg(f + PSN_FOLD_HDR + K + i) : 0.0;
-            pd[K] = cv ? __ldcg(f + 3) : 0.0;
-          }
-        } else {
-          double* pd = (double*)pr;
-          float* pf = (float*)(pr + 8 * (K + 1));
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            pd[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;  // w_q
-            pf[i] = cv ? (float)__ldg(a.W + (size_t)wr * K + i) : 0.0f;
-          }
-          pd[K] = cv ? __ldg(f + 3) : 0.0;                  // b_f
-          pf[K] = cv ? (float)__ldg(f + 0) : 0.0f;          // mu*
-          pf[K + 1] = (cv && pass == 1) ? (float)__ldcg(a.bfold + 2 * (size_t)cc) : 0.0f;
-          pf[K + 2] = (cv && pass == 1) ? (float)__ldcg(a.bfold + 2 * (size_t)cc + 1) : 0.0f;
+      const uint64_t pol_keep = pol_evict_last(), pol_drop = pol_evict_first(), pol_norm = pol_evict_normal();
+      unsigned long long tr_start = gtimer(), tr_empty = 0;
+      int q = 0;
+      auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
+        const int s = q % p.S;
+        if (q >= p.S) {
+          const unsigned long long t0 = a.trace ? gtimer() : 0;
+          mbar_wait(empty + s, (unsigned)(((q / p.S) - 1) & 1));
+          if (a.trace) tr_empty += gtimer() - t0;
         }
-        __syncwarp();
-      }
-      if (lane == 0) {
+        unsigned char* st = smem + (size_t)s * C_::STAGE;
         const uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
         const int c0 = g * kCols, n0 = nbi * kConsumerWarps;
         if (kind == kTile) {
@@ -356,44 +493,131 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load3(st, &mxh, c0, n0, trow, full + s, pol);
           tma_load3(st + C_::XBYTES, &myh, c0, n0, trow, full + s, pol);
         }
-      }
-      __syncwarp();
-      ++q;
-    };
-    for (int it = 0; it < iters; ++it) {
-      for (int pass = 0; pass < 2; ++pass) {
-        const int g = pass == 0 ? it : it - p.lag;
-        if (g < 0 || g >= p.G) continue;
-        const int v = worker_of(p, g, pass);
-        if (v >= p.P) continue;
-        if (pass == 1) {  // the fold of group g must be complete before its parameters are read
-          if (lane == 0) wait_counter(a.fdone + g, (unsigned)p.F, "fold done");
-          __syncwarp();
-        }
-        const int t_a = (int)((long long)v * p.tpg / p.P), t_b = (int)((long long)(v + 1) * p.tpg / p.P);
-        bool params = true;
-        for (int tile = t_a; tile < t_b; ++tile) {
-          const int nbi = tile / p.ttl, tt = tile % p.ttl, t0 = tt * TB;
-          if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-            issue(kHead, pass, g, nbi, t0 - H, params);
-            params = false;
+        ++q;
+      };
+      for (int it = 0; it < iters; ++it) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int g = pass == 0 ? it : it - p.lag;
+          if (g < 0 || g >= p.G) continue;
+          const int v = worker_of(p, g, pass);
+          if (v >= p.P) continue;
+          int t_a, t_b;
+          tile_range(p, v, t_a, t_b);
+          int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+          for (int tile = t_a; tile < t_b; ++tile) {
+            const int t0 = tt * TB;
+            if (H > 0 && tile == t_a && t0 > 0) issue(kHead, pass, g, nbi, t0 - H);
+            issue(kTile, pass, g, nbi, t0);
+            if (BWD && H > 0 && pass == 1 && tile == t_b - 1 && t0 + TB < p.T) issue(kTail, pass, g, nbi, t0 + TB);
+            if (++tt == p.ttl) {
+              tt = 0;
+              ++nbi;
+            }
           }
-          issue(kTile, pass, g, nbi, t0, params);
-          params = false;
-          if (BWD && H > 0 && pass == 1 && tile == t_b - 1 && t0 + TB < p.T) issue(kTail, pass, g, nbi, t0 + TB, false);
         }
       }
+      if (a.trace)
+        printf("PSNTRACE %s prod cta %d total %llu empty %llu items %d\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
+               gtimer() - tr_start, tr_empty, q);
     }
     return;
   }
 
+  if (warp == kConsumerWarps + 1) {
+    // ======================= publisher warp =======================
+    // per iteration it: (1) hand this CTA's pass-1 sums of group `it` to the
+    // grid (CTA reduction over the 8 batch-row warps in fixed order, then f64
+    // atomic adds into the group's per-channel accumulators) and arrive on the
+    // group counter -- every CTA arrives, workers or not, after reading the
+    // pre-update running statistics it will fold with; (2) for the group pass 2
+    // streams next iteration: wait until every CTA arrived, fold the 32 channels
+    // (lane = channel) into the pass-2 parameter slot.
+    unsigned long long tp_start = gtimer(), tp_dep = 0, tp_cnt = 0, tp_fold = 0;
+    int nd = 0;
+    double* prev = tot;  // [8][2][32] ring: running mean / var (pre-update) per group, forward only
+    for (int it = 0; it < iters; ++it) {
+      if (it < p.G) {
+        const int c = it * kCols + lane;
+        if (!BWD) {
+          const bool cv = c < p.C;
+          prev[((it & 7) * 2 + 0) * kCols + lane] = cv ? __ldcg(a.rm + c) : 0.0;
+          prev[((it & 7) * 2 + 1) * kCols + lane] = cv ? __ldcg(a.rv + c) : 0.0;
+        }
+        const int v = worker_of(p, it, 0);
+        if (v < p.P) {
+          const unsigned long long t0 = a.trace ? gtimer() : 0;
+          if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
+          __syncwarp();
+          if (a.trace) tp_dep += gtimer() - t0;
+          double t[NV];
+#pragma unroll
+          for (int val = 0; val < NV; ++val) {
+            double s = dep[(0 * NV + val) * kCols + lane];
+#pragma unroll
+            for (int w2 = 1; w2 < kConsumerWarps; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
+            t[val] = s;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(depe);
+#pragma unroll
+          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
+          ++nd;
+        }
+        __syncwarp();
+        if (lane == 0) red_release(a.cnt + it, 1u);
+      }
+      const int g2 = it + 1 - p.lag;  // streamed by pass 2 in iteration it + 1
+      if (g2 >= 0 && g2 < p.G) {
+        const int sl = g2 & 1;
+        unsigned long long t0 = a.trace ? gtimer() : 0;
+        if (lane == 0) wait_counter(a.cnt + g2, (unsigned)p.nCTA, "pass-1 sums");
+        __syncwarp();
+        if (a.trace) {
+          const unsigned long long t1 = gtimer();
+          tp_cnt += t1 - t0;
+          t0 = t1;
+        }
+        if (g2 >= 2) {
+          if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((g2 >> 1) - 1) & 1));
+          __syncwarp();
+        }
+        const int c = g2 * kCols + lane;
+        if (c < p.C) {
+          double tt[NV];
+#pragma unroll
+          for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g2 * NV + val) * kCols + lane);
+          const double rmp = BWD ? 0.0 : prev[((g2 & 7) * 2 + 0) * kCols + lane];
+          const double rvp = BWD ? 0.0 : prev[((g2 & 7) * 2 + 1) * kCols + lane];
+          fold_channel<K, BWD>(a, c, tt, rmp, rvp, designated_of(p, g2) == (int)blockIdx.x,
+                               p2s + sl * LY.pbytes + lane * LY.pstride);
+        } else {
+          double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
+#pragma unroll
+          for (int i = 0; i < LY.pstride / 8; ++i) pd[i] = 0.0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p2f + sl);
+        if (a.trace) tp_fold += gtimer() - t0;
+      }
+    }
+    if (a.trace && lane == 0)
+      printf("PSNTRACE %s publ cta %d total %llu dep %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd",
+             (int)blockIdx.x, gtimer() - tp_start, tp_dep, tp_cnt, tp_fold);
+    return;
+  }
+
   // ======================= consumer warps =======================
-  const int n_in = warp;  // batch row within the tile
+  constexpr int U = kRowBlock;
+  constexpr int RS = kConsumerWarps * kCols;  // elements between consecutive time rows of a box
+  const int n_in = warp;                      // batch row within the tile
   const uint64_t pol_out = pol_evict_first();
-  int q = 0;
+  int q = 0, nd = 0;
+  unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
   auto wait_item = [&]() -> unsigned char* {
     const int s = q % p.S;
+    const unsigned long long t0 = a.trace ? gtimer() : 0;
     mbar_wait(full + s, (unsigned)((q / p.S) & 1));
+    if (a.trace) tc_full += gtimer() - t0;
     return smem + (size_t)s * C_::STAGE;
   };
   auto release_item = [&]() {
@@ -401,481 +625,436 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) mbar_arrive(empty + (q % p.S));
     ++q;
   };
+  // wait for this segment's parameters; returns this lane's parameter row
+  auto take_params = [&](int g, int pass) -> const unsigned char* {
+    const int sl = g & 1;
+    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    mbar_wait((pass == 0 ? p1f : p2f) + sl, (unsigned)((g >> 1) & 1));
+    if (a.trace) tc_param += gtimer() - t0;
+    return (pass == 0 ? p1s : p2s) + sl * LY.pbytes + lane * LY.pstride;
+  };
+  auto done_params = [&](int g, int pass) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive((pass == 0 ? p1e : p2e) + (g & 1));
+  };
+  auto deposit = [&](const double* acc) {
+    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1));
+    if (a.trace) tc_dep += gtimer() - t0;
+#pragma unroll
+    for (int val = 0; val < NV; ++val) dep[(warp * NV + val) * kCols + lane] = acc[val];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(depf);
+    ++nd;
+  };
   const size_t rowstride = (size_t)p.N * p.J;
   const unsigned mN = (unsigned)p.N;
+  // pass-1 parameters are inputs of this launch (W, running mean / the forward's
+  // fold rows), so each consumer loads its column's next segment one segment ahead
+  double np1d[K + 1];
+  float np1f[K + 1];
+  auto prefetch_p1 = [&](int g) {
+    const int c = g * kCols + lane;
+    const bool cv = c < p.C;
+    const int cc = cv ? c : 0;
+    const int wr = a.shared ? 0 : cc;
+    if constexpr (!BWD) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) np1d[i] = cv ? __ldg(a.W + (size_t)wr * K + i) : 0.0;
+      np1d[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments (pre-update running mean)
+    } else {
+      const double* f = a.fold + (size_t)cc * (PSN_FOLD_HDR + 2 * K);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        np1d[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;  // w_q
+        np1f[i] = cv ? (float)__ldg(a.W + (size_t)wr * K + i) : 0.0f;
+      }
+      np1d[K] = cv ? __ldg(f + 3) : 0.0;          // b_f
+      np1f[K] = cv ? (float)__ldg(f + 0) : 0.0f;  // mu*
+    }
+  };
+  if (p.G > 0) prefetch_p1(0);
 
   for (int it = 0; it < iters; ++it) {
     // ------------------------------------------------------------- pass 1
     if (it < p.G) {
       const int g = it;
       const int v = worker_of(p, g, 0);
-      if (v < p.P) {
-        const int col = g * kCols + lane;
-        const int t_a = (int)((long long)v * p.tpg / p.P), t_b = (int)((long long)(v + 1) * p.tpg / p.P);
-        double acc[NV];
+      const int col = g * kCols + lane;
+      int t_a, t_b;
+      tile_range(p, v, t_a, t_b);
+      if (v >= p.P) t_a = t_b = 0;
+      double acc[NV];
 #pragma unroll
-        for (int u = 0; u < NV; ++u) acc[u] = 0.0;
-        if constexpr (!BWD) {
-          double w[K], sh = 0.0, xw[H + 1];
-          for (int tile = t_a; tile < t_b; ++tile) {
-            const int nbi = tile / p.ttl, tt = tile % p.ttl, t0 = tt * TB;
-            const bool lv = (unsigned)(nbi * kConsumerWarps + n_in) < mN && col < p.J;
-            if (tile == t_a || tt == 0) {
+      for (int u = 0; u < NV; ++u) acc[u] = 0.0;
+      if constexpr (!BWD) {
+        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
+        double w[K], xw[H + U], sh;
 #pragma unroll
-              for (int j = 0; j <= H; ++j) xw[j] = 0.0;
-            }
-            if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-              const unsigned char* st = wait_item();
-              if (tile == t_a) {
-                const double* pd = (const double*)(st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE);
+        for (int i = 0; i < K; ++i) w[i] = np1d[i];
+        sh = np1d[K];
+        if (g + 1 < p.G) prefetch_p1(g + 1);
+        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        for (int tile = t_a; tile < t_b; ++tile) {
+          const int t0 = tt * TB;
+          const bool lv = (unsigned)(nbi * kConsumerWarps + n_in) < mN && col < p.J;
+          if (tile == t_a || tt == 0) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) w[i] = pd[i];
-                sh = pd[K];
-              }
-              const IO* xs = (const IO*)st + n_in * kCols + lane;
-#pragma unroll
-              for (int r = 0; r < H; ++r) {
-#pragma unroll
-                for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
-                xw[H - 1] = (double)lds(xs + r * kConsumerWarps * kCols);
-              }
-              release_item();
-            }
+            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+          }
+          if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const unsigned char* st = wait_item();
-            if (tile == t_a && !(H > 0 && t0 > 0)) {
-              const double* pd = (const double*)(st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE);
-#pragma unroll
-              for (int i = 0; i < K; ++i) w[i] = pd[i];
-              sh = pd[K];
-            }
             const IO* xs = (const IO*)st + n_in * kCols + lane;
-            const int nvalid = lv ? min(TB, p.T - t0) : 0;
-            double S1 = 0.0, S2 = 0.0;
 #pragma unroll
-            for (int r = 0; r < TB; ++r) {
-              xw[H] = (double)lds(xs + r * kConsumerWarps * kCols);
-              double h = 0.0;
-#pragma unroll
-              for (int i = 0; i < K; ++i) h = fma(w[i], xw[slot<K, D>(i)], h);
-              const double h1 = round_f32(h);
-              const double hc = (r < nvalid) ? h1 - sh : 0.0;
-              S1 += hc;
-              S2 = fma(hc, hc, S2);
-#pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
-            }
-            acc[0] += S1;
-            acc[1] += S2;
+            for (int r = 0; r < H; ++r) xw[r] = (double)lds(xs + r * RS);
             release_item();
           }
-        } else {
-          // db, dw_q: f64 end to end (h2 exact and f32-rounded like the reference's
-          // carrier, sigma' and dh2 in f64) -- f32 per-element errors (~1e-7)
-          // would grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5
-          // absolute bound on small dW entries; the BN-term sums sx, sxc reach dW
-          // through 1/m-scaled factors and use f32 within a tile.
-          float w[K], mu = 0.f, xw[H + 1];
-          double wq[K], bf = 0.0, xd[H + 1];
-          for (int tile = t_a; tile < t_b; ++tile) {
-            const int nbi = tile / p.ttl, tt = tile % p.ttl, t0 = tt * TB;
-            if (tile == t_a || tt == 0) {
+          const unsigned char* st = wait_item();
+          const IO* xs = (const IO*)st + n_in * kCols + lane;
+          const int nvalid = lv ? min(TB, p.T - t0) : 0;
+          double S1[U], S2[U];
 #pragma unroll
-              for (int j = 0; j <= H; ++j) {
-                xw[j] = 0.f;
-                xd[j] = 0.0;
-              }
+          for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
+          if (!(a.dbg & 2))
+#pragma unroll
+          for (int r0 = 0; r0 < TB; r0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+            double h[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
+#pragma unroll
+            for (int i = 1; i < K; ++i)
+#pragma unroll
+              for (int u = 0; u < U; ++u) h[u] = fma(w[i], xw[u + slot<K, D>(i)], h[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const double hc = (r0 + u < nvalid) ? round_f32(h[u]) - sh : 0.0;
+              S1[u] += hc;
+              S2[u] = fma(hc, hc, S2[u]);
             }
-            auto load_params = [&](const unsigned char* st) {
-              const unsigned char* pr = st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE;
-              const double* pd = (const double*)pr;
-              const float* pf = (const float*)(pr + 8 * (K + 1));
 #pragma unroll
-              for (int i = 0; i < K; ++i) {
-                wq[i] = pd[i];
-                w[i] = pf[i];
-              }
-              bf = pd[K];
-              mu = pf[K];
-            };
-            if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-              const unsigned char* st = wait_item();
-              load_params(st);
-              const IO* xs = (const IO*)st + n_in * kCols + lane;
+            for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+          }
 #pragma unroll
-              for (int r = 0; r < H; ++r) {
+          for (int u = 0; u < U; ++u) {
+            acc[0] += S1[u];
+            acc[1] += S2[u];
+          }
+          release_item();
+          if (++tt == p.ttl) {
+            tt = 0;
+            ++nbi;
+          }
+        }
+      } else {
+        // ---- backward pass 1: db, dw_q (f64 end to end: h2 exact and f32-rounded like the
+        // reference's carrier, sigma' and dh2 in f64 -- f32 per-element errors (~1e-7) would
+        // grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5 bound on small dW
+        // entries); the BN-term sums sx, sxc reach dW through 1/m-scaled factors and use
+        // f32 within a tile.  Rows alternate between two f64 accumulator sets (ILP).
+        float w[K], xw[H + U];
+        double wq[K], xd[H + U], acc2[1 + K];
 #pragma unroll
-                for (int j = 0; j < H; ++j) {
-                  xw[j] = xw[j + 1];
-                  xd[j] = xd[j + 1];
-                }
-                xw[H - 1] = lds(xs + r * kConsumerWarps * kCols);
-                xd[H - 1] = (double)xw[H - 1];
-              }
-              release_item();
+        for (int i = 0; i <= K; ++i) acc2[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          wq[i] = np1d[i];
+          w[i] = np1f[i];
+        }
+        const double bf = np1d[K];
+        const float mu = np1f[K];
+        if (g + 1 < p.G) prefetch_p1(g + 1);
+        int tt = t_a % p.ttl;
+        for (int tile = t_a; tile < t_b; ++tile) {
+          const int t0 = tt * TB;
+          if (tile == t_a || tt == 0) {
+#pragma unroll
+            for (int j = 0; j < H + U; ++j) {
+              xw[j] = 0.f;
+              xd[j] = 0.0;
             }
+          }
+          if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const unsigned char* st = wait_item();
-            if (tile == t_a && !(H > 0 && t0 > 0)) load_params(st);
             const IO* xs = (const IO*)st + n_in * kCols + lane;
-            const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
-            const int nvalid = min(TB, p.T - t0);
-            float fsx[K], fsc[K];
 #pragma unroll
-            for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
+            for (int r = 0; r < H; ++r) {
+              xw[r] = lds(xs + r * RS);
+              xd[r] = (double)xw[r];
+            }
+            release_item();
+          }
+          const unsigned char* st = wait_item();
+          const IO* xs = (const IO*)st + n_in * kCols + lane;
+          const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
+          const int nvalid = min(TB, p.T - t0);
+          float fsx[K], fsc[K];
 #pragma unroll
-            for (int r = 0; r < TB; ++r) {
-              xw[H] = lds(xs + r * kConsumerWarps * kCols);
-              xd[H] = (double)xw[H];
-              const bool ok = r < nvalid;
-              const double yv = ok ? (double)lds(ys + r * kConsumerWarps * kCols) : 0.0;
-              double h2 = 0.0;  // exact: power-of-two products
+          for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
+          if (!(a.dbg & 2))
 #pragma unroll
-              for (int i = 0; i < K; ++i) h2 = fma(wq[i], xd[slot<K, D>(i)], h2);
-              h2 = round_f32(__dadd_rn(h2, bf));
-              const double tq = a.sc * h2;
-              const double den = fma(tq, a.skind == PSN_ARCTAN ? tq : h2, 1.0);
-              const double dh = yv * rcp_f64(den);  // dh2 / scale (scale applied in the fold)
-              acc[0] += dh;
+          for (int r0 = 0; r0 < TB; r0 += U) {
+            double yv[U], h2[U], dh[U];
 #pragma unroll
-              for (int i = 0; i < K; ++i) acc[1 + i] = fma(xd[slot<K, D>(i)], dh, acc[1 + i]);
-              float h1 = 0.f;
+            for (int u = 0; u < U; ++u) {
+              xw[H + u] = lds(xs + (r0 + u) * RS);
+              xd[H + u] = (double)xw[H + u];
+              yv[u] = (r0 + u < nvalid) ? (double)lds(ys + (r0 + u) * RS) : 0.0;
+            }
 #pragma unroll
-              for (int i = 0; i < K; ++i) h1 = fmaf(w[i], xw[slot<K, D>(i)], h1);
+            for (int u = 0; u < U; ++u) h2[u] = wq[0] * xd[u + slot<K, D>(0)];  // exact products
+#pragma unroll
+            for (int i = 1; i < K; ++i)
+#pragma unroll
+              for (int u = 0; u < U; ++u) h2[u] = fma(wq[i], xd[u + slot<K, D>(i)], h2[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const double h = round_f32(__dadd_rn(h2[u], bf));
+              const double tq = a.sc * h;
+              const double den = fma(tq, a.skind == PSN_ARCTAN ? tq : h, 1.0);
+              dh[u] = yv[u] * rcp_f64(den);  // dh2 / scale (scale applied in the fold)
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              double* A = (u & 1) ? acc2 : acc;
+              A[0] += dh[u];
+#pragma unroll
+              for (int i = 0; i < K; ++i) A[1 + i] = fma(xd[u + slot<K, D>(i)], dh[u], A[1 + i]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              float h1 = w[0] * xw[u + slot<K, D>(0)];
+#pragma unroll
+              for (int i = 1; i < K; ++i) h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
+              const bool ok = r0 + u < nvalid;
               const float hc = ok ? h1 - mu : 0.f;
               const float okf = ok ? 1.f : 0.f;
 #pragma unroll
               for (int i = 0; i < K; ++i) {
-                const float xi = xw[slot<K, D>(i)];
+                const float xi = xw[u + slot<K, D>(i)];
                 fsx[i] = fmaf(xi, okf, fsx[i]);
                 fsc[i] = fmaf(xi, hc, fsc[i]);
               }
-#pragma unroll
-              for (int j = 0; j < H; ++j) {
-                xw[j] = xw[j + 1];
-                xd[j] = xd[j + 1];
-              }
             }
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              acc[1 + K + i] += (double)fsx[i];
-              acc[1 + 2 * K + i] += (double)fsc[i];
+            for (int j = 0; j < H; ++j) {
+              xw[j] = xw[j + U];
+              xd[j] = xd[j + U];
             }
-            release_item();
           }
-        }
-        // ---- CTA reduction over the 8 batch rows, fixed order; one slot per worker
 #pragma unroll
-        for (int v0 = 0; v0 < NV; v0 += 8) {
-          consumer_sync();
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (v0 + u < NV) red[(warp * 8 + u) * 32 + lane] = acc[v0 + u];
-          consumer_sync();
-          if (v0 + warp < NV) {
-            double t = red[(0 * 8 + warp) * 32 + lane];
-#pragma unroll
-            for (int w2 = 1; w2 < kConsumerWarps; ++w2) t += red[(w2 * 8 + warp) * 32 + lane];
-            a.part[(((size_t)g * NV + v0 + warp) * kCols + lane) * p.P + v] = t;
+          for (int i = 0; i < K; ++i) {
+            acc[1 + K + i] += (double)fsx[i];
+            acc[1 + 2 * K + i] += (double)fsc[i];
           }
+          release_item();
+          if (++tt == p.ttl) tt = 0;
         }
-        consumer_sync();
-        if (threadIdx.x == 0) red_release(a.cnt + g, 1u);
+#pragma unroll
+        for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
       }
-    }
-    // ------------------------------------------------------------- fold of group it-1
-    if (it >= 1 && it - 1 < p.G) {
-      const int g = it - 1;
-      for (int f = 0; f < p.F; ++f) {
-        if (folder_of(p, g, f) != (int)blockIdx.x) continue;
-        consumer_sync();  // `red` is free
-        if (threadIdx.x == 0) wait_counter(a.cnt + g, (unsigned)p.P, "pass-1 partials");
-        consumer_sync();
-        const int cpf = kCols / p.F;
-        const int ntask = cpf * NV;
-        const int qn = (p.P + 31) / 32;
-        double* tot = red;  // [cpf][NV]
-        for (int tb = warp * 4; tb < ntask; tb += kConsumerWarps * 4) {
-          double sums[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int task = tb + u;
-            double s = 0.0;
-            if (task < ntask) {
-              const int chl = f * cpf + task / NV, val = task % NV;
-              const double* src = a.part + (((size_t)g * NV + val) * kCols + chl) * p.P;
-              double vals[5];
-#pragma unroll
-              for (int j = 0; j < 5; ++j) {
-                const int vv = lane + 32 * j;
-                vals[j] = (j < qn && vv < p.P) ? __ldcg(src + vv) : 0.0;
-              }
-#pragma unroll
-              for (int j = 0; j < 5; ++j) s += vals[j];
-            }
-            sums[u] = s;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const double o = __shfl_xor_sync(0xffffffffu, sums[u], off);
-              sums[u] = (lane & off) ? o + sums[u] : sums[u] + o;
-            }
-            if (lane == 0 && tb + u < ntask) tot[tb + u] = sums[u];
-          }
-        }
-        consumer_sync();
-        if ((int)threadIdx.x < cpf) {
-          const int c = g * kCols + f * cpf + threadIdx.x;
-          if (c < p.C) {
-            const double* tt = tot + threadIdx.x * NV;
-            const double* Wc = a.W + (a.shared ? 0 : (size_t)c * K);
-            double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
-            const int flags = a.flags;
-            const double m = (double)p.T * (double)p.N;
-            if constexpr (!BWD) {
-              const bool smooth = flags & PSN_SMOOTH;
-              const bool use_batch = flags & PSN_USE_BATCH_STATS;
-              const bool quantize = (flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH));
-              const double rm_prev = a.rm[c], rv_prev = a.rv[c];
-              const double dmean = tt[0] / m;
-              const double mu_b = rm_prev + dmean;  // the pass-1 shift was running_mean (pre-update)
-              double var_b = tt[1] / m - dmean * dmean;
-              var_b = var_b < 0.0 ? 0.0 : var_b;
-              if (!smooth) {  // network.py:241-248
-                const double unbiased = m > 1.0 ? var_b * (m / (m - 1.0)) : var_b;
-                double r1 = rm_prev * (1.0 - a.momentum);
-                r1 = r1 + a.momentum * mu_b;
-                double r2 = rv_prev * (1.0 - a.momentum);
-                r2 = r2 + a.momentum * unbiased;
-                a.rm[c] = r1;
-                a.rv[c] = r2;
-              }
-              const double mu = use_batch ? mu_b : rm_prev;  // network.py:250-255
-              const double var = use_batch ? var_b : rv_prev;
-              const double s = sqrt(var + a.eps);
-              const double aa = a.gamma[c] / s;
-              fr[0] = mu;
-              fr[1] = s;
-              fr[2] = aa;
-              fr[3] = a.beta[c] - aa * mu;
-              fr[4] = mu_b;
-              fr[5] = var_b;
-              for (int i = 0; i < K; ++i) {
-                const double wf = aa * Wc[i];
-                fr[PSN_FOLD_HDR + i] = wf;
-                double wq = wf;
-                if (quantize) {
-                  int sg, e;
-                  quantize_pow2(wf, sg, e);
-                  wq = ldexp((double)sg, e);
-                }
-                fr[PSN_FOLD_HDR + K + i] = wq;
-              }
-            } else {
-              const double mu = fr[0], s = fr[1], aa = fr[2];
-              const bool quantized =
-                  (flags & PSN_QUANTIZED) && (!(flags & PSN_SMOOTH) || (flags & PSN_QUANTIZE_IN_SMOOTH));
-              const double db_f = tt[0] * a.sscale;
-              double da = 0.0, dwf[K];
-              for (int i = 0; i < K; ++i) {  // quantize_backward, quant.py:194-216
-                double g1 = tt[1 + i] * a.sscale;
-                if (quantized && (flags & PSN_ROUND_STE)) {
-                  const double wf = fr[PSN_FOLD_HDR + i], wq = fr[PSN_FOLD_HDR + K + i];
-                  g1 = (wf != 0.0) ? g1 * (fabs(wq) / fabs(wf)) : 0.0;
-                }
-                dwf[i] = g1;
-                da = da + dwf[i] * Wc[i];
-              }
-              da = da - db_f * mu;  // network.py:291-296
-              double alpha1 = 0.0, beta1 = 0.0;
-              if (flags & PSN_USE_BATCH_STATS) {  // network.py:298-315
-                const double ds = -da * a.gamma[c] / (s * s);
-                const double dvar = ds / (2.0 * s);
-                const double dmu = -db_f * aa;
-                alpha1 = dmu / m;
-                beta1 = (2.0 / m) * dvar;
-              }
-              for (int i = 0; i < K; ++i) {
-                double dw = aa * dwf[i];
-                if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * tt[1 + K + i] + beta1 * tt[1 + 2 * K + i];
-                a.dW[(size_t)c * K + i] = dw;
-              }
-              a.dbeta[c] = db_f;
-              a.dgamma[c] = da / s;
-              a.bfold[2 * (size_t)c] = alpha1;
-              a.bfold[2 * (size_t)c + 1] = beta1;
-            }
-          }
-        }
-        consumer_sync();
-        if (threadIdx.x == 0) red_release(a.fdone + g, 1u);
-      }
+      if (v < p.P) deposit(acc);  // CTA reduction + publication happen on the publisher warp
     }
     // ------------------------------------------------------------- pass 2
     if (it >= p.lag && it - p.lag < p.G) {
       const int g = it - p.lag;
       const int v = worker_of(p, g, 1);
-      if (v < p.P) {
-        const int col = g * kCols + lane;
-        const int t_a = (int)((long long)v * p.tpg / p.P), t_b = (int)((long long)(v + 1) * p.tpg / p.P);
-        IO* out = (IO*)a.out;
-        if constexpr (!BWD) {
-          double wq[K], bf = 0.0, xw[H + 1];
-          for (int tile = t_a; tile < t_b; ++tile) {
-            const int nbi = tile / p.ttl, tt = tile % p.ttl, t0 = tt * TB;
-            const int n = nbi * kConsumerWarps + n_in;
-            const bool lv = (unsigned)n < mN && col < p.J;
-            if (tile == t_a || tt == 0) {
+      const unsigned char* pr = take_params(g, 1);
+      const int col = g * kCols + lane;
+      int t_a, t_b;
+      tile_range(p, v, t_a, t_b);
+      if (v >= p.P) t_a = t_b = 0;
+      IO* out = (IO*)a.out;
+      if constexpr (!BWD) {
+        // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
+        double wq[K], xw[H + U];
+        const double* pd = (const double*)pr;
 #pragma unroll
-              for (int j = 0; j <= H; ++j) xw[j] = 0.0;
-            }
-            auto load_params = [&](const unsigned char* st) {
-              const double* pd = (const double*)(st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE);
+        for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
+        const double bf = ldsd(pd + K);
+        done_params(g, 1);
+        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        for (int tile = t_a; tile < t_b; ++tile) {
+          const int t0 = tt * TB;
+          const int n = nbi * kConsumerWarps + n_in;
+          const bool lv = (unsigned)n < mN && col < p.J;
+          if (tile == t_a || tt == 0) {
 #pragma unroll
-              for (int i = 0; i < K; ++i) wq[i] = pd[i];
-              bf = pd[K];
-            };
-            if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-              const unsigned char* st = wait_item();
-              load_params(st);
-              const IO* xs = (const IO*)st + n_in * kCols + lane;
-#pragma unroll
-              for (int r = 0; r < H; ++r) {
-#pragma unroll
-                for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
-                xw[H - 1] = (double)lds(xs + r * kConsumerWarps * kCols);
-              }
-              release_item();
-            }
+            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+          }
+          if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const unsigned char* st = wait_item();
-            if (tile == t_a && !(H > 0 && t0 > 0)) load_params(st);
             const IO* xs = (const IO*)st + n_in * kCols + lane;
-            const int nvalid = lv ? min(TB, p.T - t0) : 0;
-            IO* o = out + ((size_t)t0 * mN + (lv ? n : 0)) * p.J + (lv ? col : 0);
 #pragma unroll
-            for (int r = 0; r < TB; ++r) {
-              xw[H] = (double)lds(xs + r * kConsumerWarps * kCols);
-              double h = 0.0;  // power-of-two products are exact: DFMA == the reference's mul-then-add
-#pragma unroll
-              for (int i = 0; i < K; ++i) h = fma(wq[i], xw[slot<K, D>(i)], h);
-              h = __dadd_rn(h, bf);
-              // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
-              const float sp = h >= -0x1p-150 ? 1.0f : 0.0f;
-              if (r < nvalid) st_out(o + (size_t)r * rowstride, sp, pol_out);
-#pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
-            }
+            for (int r = 0; r < H; ++r) xw[r] = (double)lds(xs + r * RS);
             release_item();
           }
-        } else {
-          float w[K], wq[K], bf = 0.f, mu = 0.f, a1 = 0.f, b1 = 0.f, xw[H + 1], pacc[H + 1];
-          int run_t0 = 0;
-          bool lv = false;
-          IO* obase = out;
-          // one time step of the transposed conv: scatter this step's dh into the
-          // H+1-slot ring, then emit dx for the step H behind (now complete)
-          auto step = [&](float xv, float yv, bool ok, int tcur) {
-            xw[H] = xv;
-            float h1 = 0.f, h2 = 0.f;
+          const unsigned char* st = wait_item();
+          const IO* xs = (const IO*)st + n_in * kCols + lane;
+          const int nvalid = lv ? min(TB, p.T - t0) : 0;
+          IO* o = out + ((size_t)t0 * mN + (lv ? n : 0)) * p.J + (lv ? col : 0);
+          if (!(a.dbg & 4))
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              h1 = fmaf(w[i], xw[slot<K, D>(i)], h1);
-              h2 = fmaf(wq[i], xw[slot<K, D>(i)], h2);
+          for (int r0 = 0; r0 < TB; r0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+            double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
+#pragma unroll
+            for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
+#pragma unroll
+            for (int i = 1; i < K; ++i)
+#pragma unroll
+              for (int u = 0; u < U; ++u) h[u] = fma(wq[i], xw[u + slot<K, D>(i)], h[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
+              const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
+              if (r0 + u < nvalid && !(a.dbg & 1)) st_out(o + (size_t)(r0 + u) * rowstride, sp, pol_out);
             }
-            h2 += bf;
-            const float dh2 = ok ? yv * surrogate_grad(a.sur, h2) : 0.f;
-            const float dh1 = ok ? fmaf(b1, h1 - mu, a1) : 0.f;
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              pacc[slot<K, D>(i)] = fmaf(wq[i], dh2, pacc[slot<K, D>(i)]);
-              pacc[slot<K, D>(i)] = fmaf(w[i], dh1, pacc[slot<K, D>(i)]);
-            }
-            const int od = tcur - H;
-            if (lv && od >= run_t0 && od < p.T) st_out(obase + (size_t)od * rowstride, pacc[0], pol_out);
+            for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+          }
+          release_item();
+          if (++tt == p.ttl) {
+            tt = 0;
+            ++nbi;
+          }
+        }
+      } else {
+        // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
+        // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
+        // partial dx of row t_blk - H + j; after a block of U rows the first U slots
+        // are complete)
+        float w[K], wq[K], xw[H + U], pacc[H + U];
+        const double* pd = (const double*)pr;
+        const float* pf = (const float*)(pr + 8 * (K + 1));
 #pragma unroll
-            for (int j = 0; j < H; ++j) {
-              pacc[j] = pacc[j + 1];
-              xw[j] = xw[j + 1];
-            }
-            pacc[H] = 0.f;
-          };
-          auto drain = [&](int tnext) {  // the stream ended at T: flush the ring
+        for (int i = 0; i < K; ++i) {
+          wq[i] = (float)ldsd(pd + i);
+          w[i] = ldsf(pf + i);
+        }
+        const float bf = (float)ldsd(pd + K);
+        const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);
+        done_params(g, 1);
+        int run_t0 = 0;
+        bool lv = false;
+        IO* obase = out;
+        auto emit = [&](int od, float val) {
+          if (lv && od >= run_t0 && od < p.T && !(a.dbg & 1)) st_out(obase + (size_t)od * rowstride, val, pol_out);
+        };
+        auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1) {
+          float h1 = w[0] * xw[u + slot<K, D>(0)], h2 = wq[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
-            for (int s2 = 0; s2 < H; ++s2) {
-              const int od = tnext + s2 - H;
-              if (lv && od >= run_t0 && od < p.T) st_out(obase + (size_t)od * rowstride, pacc[0], pol_out);
+          for (int i = 1; i < K; ++i) {
+            h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
+            h2 = fmaf(wq[i], xw[u + slot<K, D>(i)], h2);
+          }
+          h2 += bf;
+          dh2 = ok ? yv * surrogate_grad(a.sur, h2) : 0.f;
+          dh1 = ok ? fmaf(b1, h1 - mu, a1) : 0.f;
+        };
+        // single-row step (TAIL rows): scatter, emit the row H behind, shift by one
+        auto step1 = [&](float xv, float yv, bool ok, int tcur) {
+          xw[H] = xv;
+          float dh2, dh1;
+          dh_row(0, yv, ok, dh2, dh1);
 #pragma unroll
-              for (int j = 0; j < H; ++j) pacc[j] = pacc[j + 1];
-              pacc[H] = 0.f;
-            }
-          };
-          auto load_params = [&](const unsigned char* st) {
-            const unsigned char* pr = st + C_::XBYTES + C_::DBYTES + lane * C_::PSTRIDE;
-            const double* pd = (const double*)pr;
-            const float* pf = (const float*)(pr + 8 * (K + 1));
+          for (int i = 0; i < K; ++i) {
+            pacc[slot<K, D>(i)] = fmaf(wq[i], dh2, pacc[slot<K, D>(i)]);
+            pacc[slot<K, D>(i)] = fmaf(w[i], dh1, pacc[slot<K, D>(i)]);
+          }
+          emit(tcur - H, pacc[0]);
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              wq[i] = (float)pd[i];
-              w[i] = pf[i];
-            }
-            bf = (float)pd[K];
-            mu = pf[K];
-            a1 = pf[K + 1];
-            b1 = pf[K + 2];
-          };
-          for (int tile = t_a; tile < t_b; ++tile) {
-            const int nbi = tile / p.ttl, tt = tile % p.ttl, t0 = tt * TB;
-            if (tile == t_a || tt == 0) {
-              const int n = nbi * kConsumerWarps + n_in;
-              lv = (unsigned)n < mN && col < p.J;
-              obase = out + (size_t)(lv ? n : 0) * p.J + (lv ? col : 0);
-              run_t0 = t0;
+          for (int j = 0; j < H + U - 1; ++j) pacc[j] = pacc[j + 1];
+          pacc[H + U - 1] = 0.f;
 #pragma unroll
-              for (int j = 0; j <= H; ++j) xw[j] = pacc[j] = 0.f;
-            }
-            if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-              const unsigned char* st = wait_item();
-              load_params(st);
-              const IO* xs = (const IO*)st + n_in * kCols + lane;
+          for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
+        };
+        auto drain = [&](int tnext) {  // the stream ended at T: flush the ring
 #pragma unroll
-              for (int r = 0; r < H; ++r) {
+          for (int s2 = 0; s2 < H; ++s2) {
+            emit(tnext + s2 - H, pacc[0]);
 #pragma unroll
-                for (int j = 0; j < H; ++j) xw[j] = xw[j + 1];
-                xw[H - 1] = lds(xs + r * kConsumerWarps * kCols);
+            for (int j = 0; j < H + U - 1; ++j) pacc[j] = pacc[j + 1];
+            pacc[H + U - 1] = 0.f;
+          }
+        };
+        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        for (int tile = t_a; tile < t_b; ++tile) {
+          const int t0 = tt * TB;
+          if (tile == t_a || tt == 0) {
+            const int n = nbi * kConsumerWarps + n_in;
+            lv = (unsigned)n < mN && col < p.J;
+            obase = out + (size_t)(lv ? n : 0) * p.J + (lv ? col : 0);
+            run_t0 = t0;
+#pragma unroll
+            for (int j = 0; j < H + U; ++j) xw[j] = pacc[j] = 0.f;
+          }
+          if constexpr (H > 0) if (tile == t_a && t0 > 0) {
+            const unsigned char* st = wait_item();
+            const IO* xs = (const IO*)st + n_in * kCols + lane;
+#pragma unroll
+            for (int r = 0; r < H; ++r) xw[r] = lds(xs + r * RS);
+            release_item();
+          }
+          const unsigned char* st = wait_item();
+          {
+            const IO* xs = (const IO*)st + n_in * kCols + lane;
+            const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
+            const int nvalid = min(TB, p.T - t0);
+            if (!(a.dbg & 4))
+#pragma unroll
+            for (int r0 = 0; r0 < TB; r0 += U) {
+              float dh2[U], dh1[U];
+#pragma unroll
+              for (int u = 0; u < U; ++u) xw[H + u] = lds(xs + (r0 + u) * RS);
+#pragma unroll
+              for (int u = 0; u < U; ++u) dh_row(u, lds(ys + (r0 + u) * RS), r0 + u < nvalid, dh2[u], dh1[u]);
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  pacc[u + slot<K, D>(i)] = fmaf(wq[i], dh2[u], pacc[u + slot<K, D>(i)]);
+                  pacc[u + slot<K, D>(i)] = fmaf(w[i], dh1[u], pacc[u + slot<K, D>(i)]);
+                }
+#pragma unroll
+              for (int u = 0; u < U; ++u) emit(t0 + r0 + u - H, pacc[u]);
+#pragma unroll
+              for (int j = 0; j < H; ++j) {
+                pacc[j] = pacc[j + U];
+                xw[j] = xw[j + U];
               }
+#pragma unroll
+              for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
+            }
+          }
+          release_item();
+          if constexpr (H > 0) {
+            if (t0 + TB >= p.T) {
+              drain(t0 + TB);
+            } else if (tile == t_b - 1) {  // range ends mid-stream: future dh from the TAIL rows
+              const unsigned char* st2 = wait_item();
+              const IO* xs = (const IO*)st2 + n_in * kCols + lane;
+              const IO* ys = (const IO*)(st2 + C_::XBYTES) + n_in * kCols + lane;
+              const int te = t0 + TB;
+              const int nvalid = min(H, p.T - te);
+#pragma unroll
+              for (int r = 0; r < H; ++r) step1(lds(xs + r * RS), lds(ys + r * RS), r < nvalid, te + r);
               release_item();
             }
-            const unsigned char* st = wait_item();
-            if (tile == t_a && !(H > 0 && t0 > 0)) load_params(st);
-            {
-              const IO* xs = (const IO*)st + n_in * kCols + lane;
-              const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
-              const int nvalid = min(TB, p.T - t0);
-#pragma unroll
-              for (int r = 0; r < TB; ++r)
-                step(lds(xs + r * kConsumerWarps * kCols), lds(ys + r * kConsumerWarps * kCols), r < nvalid, t0 + r);
-            }
-            release_item();
-            if constexpr (H > 0) {
-              if (t0 + TB >= p.T) {
-                drain(t0 + TB);
-              } else if (tile == t_b - 1) {  // range ends mid-stream: future dh from the TAIL rows
-                const unsigned char* st2 = wait_item();
-                const IO* xs = (const IO*)st2 + n_in * kCols + lane;
-                const IO* ys = (const IO*)(st2 + C_::XBYTES) + n_in * kCols + lane;
-                const int te = t0 + TB;
-                const int nvalid = min(H, p.T - te);
-#pragma unroll
-                for (int r = 0; r < H; ++r)
-                  step(lds(xs + r * kConsumerWarps * kCols), lds(ys + r * kConsumerWarps * kCols), r < nvalid, te + r);
-                release_item();
-              }
-            }
+          }
+          if (++tt == p.ttl) {
+            tt = 0;
+            ++nbi;
           }
         }
       }
     }
   }
+  if (a.trace && threadIdx.x == 0)
+    printf("PSNTRACE %s cons cta %d total %llu full %llu param %llu dep %llu items %d\n", BWD ? "bwd" : "fwd",
+           (int)blockIdx.x, gtimer() - tc_start, tc_full, tc_param, tc_dep, q);
 }
 
 // -------------------------------------------------------------------------
@@ -889,7 +1068,7 @@ int stream_launch(const Args& args, const void* x, const void* dy, cudaStream_t 
   CUtensorMap maps[4];
   int rc = stream_encode_maps(args.p, (int)sizeof(IO), BWD, x, dy, maps);
   if (rc) return rc;
-  const size_t smem = (size_t)args.p.S * C_::STAGE + kRedBytes + 16 * (size_t)args.p.S + 1024;
+  const size_t smem = (size_t)args.p.S * C_::STAGE + C_::L.fixed + 16 * (size_t)args.p.S + 1024;
   auto kern = psn_stream_kernel<K, D, IO, BWD>;
   cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (stream kernel smem) failed");
@@ -903,11 +1082,6 @@ int stream_launch(const Args& args, const void* x, const void* dy, cudaStream_t 
     return fail(PSN_ERR_CUDA, buf);
   }
   return PSN_OK;
-}
-
-template <int K, int D, typename IO, bool BWD>
-constexpr int stage_bytes() {
-  return Cfg<K, D, IO, BWD>::STAGE;
 }
 
 }  // namespace stream
