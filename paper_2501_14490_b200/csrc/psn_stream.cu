@@ -163,7 +163,6 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
   a.eps = desc->eps;
   a.momentum = desc->momentum;
   a.trace = env_int("PSN_TRACE", 0);
-  a.dbg = env_int("PSN_DBG", 0);
   return dispatch(desc, false, a, x, nullptr, st);
 }
 
@@ -190,7 +189,6 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
   a.eps = desc->eps;
   a.momentum = desc->momentum;
   a.trace = env_int("PSN_TRACE", 0);
-  a.dbg = env_int("PSN_DBG", 0);
   Surrogate s;
   s.kind = desc->surrogate;
   if (desc->surrogate == PSN_ARCTAN) {

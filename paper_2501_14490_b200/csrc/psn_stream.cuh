@@ -92,7 +92,6 @@ struct Args {
   int shared;
   double eps, momentum;
   Surrogate sur;    // f32 surrogate (dx pass)
-  int dbg;           // PSN_DBG ablation mask (benchmarking only): 1 skip stores, 2 skip pass-1 math, 4 skip pass-2 math
   int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
   double sc, sscale; // f64 surrogate: arctan c = pi*alpha/2, scale = alpha/2; rational c = alpha, scale = 1
   int skind;
@@ -711,30 +710,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const unsigned char* st = wait_item();
           const IO* xs = (const IO*)st + n_in * kCols + lane;
-          const int nvalid = lv ? min(TB, p.T - t0) : 0;
+          const int nvalid = min(TB, p.T - t0);
           double S1[U], S2[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
-          if (!(a.dbg & 2))
+          // full tiles (every row < T) run without per-row predicates
+          auto rows = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-          for (int r0 = 0; r0 < TB; r0 += U) {
+            for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
-            double h[U];
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+              double h[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
+              for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
-            for (int i = 1; i < K; ++i)
+              for (int i = 1; i < K; ++i)
 #pragma unroll
-              for (int u = 0; u < U; ++u) h[u] = fma(w[i], xw[u + slot<K, D>(i)], h[u]);
+                for (int u = 0; u < U; ++u) h[u] = fma(w[i], xw[u + slot<K, D>(i)], h[u]);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const double hc = (r0 + u < nvalid) ? round_f32(h[u]) - sh : 0.0;
-              S1[u] += hc;
-              S2[u] = fma(hc, hc, S2[u]);
+              for (int u = 0; u < U; ++u) {
+                double hc = round_f32(h[u]) - sh;
+                if (!FULL) hc = (r0 + u < nvalid) ? hc : 0.0;
+                S1[u] += hc;
+                S2[u] = fma(hc, hc, S2[u]);
+              }
+#pragma unroll
+              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
+          };
+          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if (!lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
 #pragma unroll
-            for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+            for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -792,57 +800,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           float fsx[K], fsc[K];
 #pragma unroll
           for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
-          if (!(a.dbg & 2))
+          auto rows = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-          for (int r0 = 0; r0 < TB; r0 += U) {
-            double yv[U], h2[U], dh[U];
+            for (int r0 = 0; r0 < TB; r0 += U) {
+              double yv[U], h2[U], dh[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              xw[H + u] = lds(xs + (r0 + u) * RS);
-              xd[H + u] = (double)xw[H + u];
-              yv[u] = (r0 + u < nvalid) ? (double)lds(ys + (r0 + u) * RS) : 0.0;
-            }
+              for (int u = 0; u < U; ++u) {
+                xw[H + u] = lds(xs + (r0 + u) * RS);
+                xd[H + u] = (double)xw[H + u];
+                yv[u] = (double)lds(ys + (r0 + u) * RS);  // rows >= T: TMA zero fill -> dh2 = 0
+              }
 #pragma unroll
-            for (int u = 0; u < U; ++u) h2[u] = wq[0] * xd[u + slot<K, D>(0)];  // exact products
+              for (int u = 0; u < U; ++u) h2[u] = wq[0] * xd[u + slot<K, D>(0)];  // exact products
 #pragma unroll
-            for (int i = 1; i < K; ++i)
+              for (int i = 1; i < K; ++i)
 #pragma unroll
-              for (int u = 0; u < U; ++u) h2[u] = fma(wq[i], xd[u + slot<K, D>(i)], h2[u]);
+                for (int u = 0; u < U; ++u) h2[u] = fma(wq[i], xd[u + slot<K, D>(i)], h2[u]);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const double h = round_f32(__dadd_rn(h2[u], bf));
-              const double tq = a.sc * h;
-              const double den = fma(tq, a.skind == PSN_ARCTAN ? tq : h, 1.0);
-              dh[u] = yv[u] * rcp_f64(den);  // dh2 / scale (scale applied in the fold)
-            }
+              for (int u = 0; u < U; ++u) {
+                const double h = round_f32(__dadd_rn(h2[u], bf));
+                const double tq = a.sc * h;
+                const double den = fma(tq, a.skind == PSN_ARCTAN ? tq : h, 1.0);
+                dh[u] = yv[u] * rcp_f64(den);  // dh2 / scale (scale applied in the fold)
+              }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              double* A = (u & 1) ? acc2 : acc;
-              A[0] += dh[u];
+              for (int u = 0; u < U; ++u) {
+                double* A = (u & 1) ? acc2 : acc;
+                A[0] += dh[u];
 #pragma unroll
-              for (int i = 0; i < K; ++i) A[1 + i] = fma(xd[u + slot<K, D>(i)], dh[u], A[1 + i]);
-            }
+                for (int i = 0; i < K; ++i) A[1 + i] = fma(xd[u + slot<K, D>(i)], dh[u], A[1 + i]);
+              }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              float h1 = w[0] * xw[u + slot<K, D>(0)];
+              for (int u = 0; u < U; ++u) {
+                float h1 = w[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
-              for (int i = 1; i < K; ++i) h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
-              const bool ok = r0 + u < nvalid;
-              const float hc = ok ? h1 - mu : 0.f;
-              const float okf = ok ? 1.f : 0.f;
+                for (int i = 1; i < K; ++i) h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
+                float hc = h1 - mu;
+                if (!FULL && !(r0 + u < nvalid)) hc = 0.f;
 #pragma unroll
-              for (int i = 0; i < K; ++i) {
-                const float xi = xw[u + slot<K, D>(i)];
-                fsx[i] = fmaf(xi, okf, fsx[i]);
-                fsc[i] = fmaf(xi, hc, fsc[i]);
+                for (int i = 0; i < K; ++i) {
+                  const float xi = xw[u + slot<K, D>(i)];
+                  if (FULL)
+                    fsx[i] += xi;
+                  else
+                    fsx[i] = (r0 + u < nvalid) ? fsx[i] + xi : fsx[i];
+                  fsc[i] = fmaf(xi, hc, fsc[i]);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < H; ++j) {
+                xw[j] = xw[j + U];
+                xd[j] = xd[j + U];
               }
             }
-#pragma unroll
-            for (int j = 0; j < H; ++j) {
-              xw[j] = xw[j + U];
-              xd[j] = xd[j + U];
-            }
-          }
+          };
+          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             acc[1 + K + i] += (double)fsx[i];
@@ -892,29 +905,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const unsigned char* st = wait_item();
           const IO* xs = (const IO*)st + n_in * kCols + lane;
-          const int nvalid = lv ? min(TB, p.T - t0) : 0;
+          const int nvalid = min(TB, p.T - t0);
           IO* o = out + ((size_t)t0 * mN + (lv ? n : 0)) * p.J + (lv ? col : 0);
-          if (!(a.dbg & 4))
+          auto rows = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-          for (int r0 = 0; r0 < TB; r0 += U) {
+            for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
-            double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+              double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
 #pragma unroll
-            for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
+              for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
-            for (int i = 1; i < K; ++i)
+              for (int i = 1; i < K; ++i)
 #pragma unroll
-              for (int u = 0; u < U; ++u) h[u] = fma(wq[i], xw[u + slot<K, D>(i)], h[u]);
+                for (int u = 0; u < U; ++u) h[u] = fma(wq[i], xw[u + slot<K, D>(i)], h[u]);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
-              const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-              if (r0 + u < nvalid && !(a.dbg & 1)) st_out(o + (size_t)(r0 + u) * rowstride, sp, pol_out);
+              for (int u = 0; u < U; ++u) {
+                // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
+                const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
+                if (lv && (FULL || r0 + u < nvalid)) st_out(o + (size_t)(r0 + u) * rowstride, sp, pol_out);
+              }
+#pragma unroll
+              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
-#pragma unroll
-            for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
-          }
+          };
+          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
@@ -941,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool lv = false;
         IO* obase = out;
         auto emit = [&](int od, float val) {
-          if (lv && od >= run_t0 && od < p.T && !(a.dbg & 1)) st_out(obase + (size_t)od * rowstride, val, pol_out);
+          if (lv && od >= run_t0 && od < p.T) st_out(obase + (size_t)od * rowstride, val, pol_out);
         };
         auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1) {
           float h1 = w[0] * xw[u + slot<K, D>(0)], h2 = wq[0] * xw[u + slot<K, D>(0)];
@@ -1003,31 +1019,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             const IO* xs = (const IO*)st + n_in * kCols + lane;
             const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
             const int nvalid = min(TB, p.T - t0);
-            if (!(a.dbg & 4))
+            const bool first = t0 == run_t0;  // rows t0-H..t0-1 of the ring belong to the previous range
+            auto rows = [&](auto full_tag) {
+              constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-            for (int r0 = 0; r0 < TB; r0 += U) {
-              float dh2[U], dh1[U];
+              for (int r0 = 0; r0 < TB; r0 += U) {
+                float dh2[U], dh1[U];
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = lds(xs + (r0 + u) * RS);
+                for (int u = 0; u < U; ++u) xw[H + u] = lds(xs + (r0 + u) * RS);
 #pragma unroll
-              for (int u = 0; u < U; ++u) dh_row(u, lds(ys + (r0 + u) * RS), r0 + u < nvalid, dh2[u], dh1[u]);
+                for (int u = 0; u < U; ++u)
+                  dh_row(u, lds(ys + (r0 + u) * RS), FULL || r0 + u < nvalid, dh2[u], dh1[u]);
 #pragma unroll
-              for (int u = 0; u < U; ++u)
+                for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  pacc[u + slot<K, D>(i)] = fmaf(wq[i], dh2[u], pacc[u + slot<K, D>(i)]);
-                  pacc[u + slot<K, D>(i)] = fmaf(w[i], dh1[u], pacc[u + slot<K, D>(i)]);
+                  for (int i = 0; i < K; ++i) {
+                    pacc[u + slot<K, D>(i)] = fmaf(wq[i], dh2[u], pacc[u + slot<K, D>(i)]);
+                    pacc[u + slot<K, D>(i)] = fmaf(w[i], dh1[u], pacc[u + slot<K, D>(i)]);
+                  }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                  const int od = t0 + r0 + u - H;  // complete now
+                  const bool ok = lv && (r0 + u >= H || !first) && (FULL || od < p.T);
+                  if (ok) st_out(obase + (size_t)od * rowstride, pacc[u], pol_out);
                 }
 #pragma unroll
-              for (int u = 0; u < U; ++u) emit(t0 + r0 + u - H, pacc[u]);
+                for (int j = 0; j < H; ++j) {
+                  pacc[j] = pacc[j + U];
+                  xw[j] = xw[j + U];
+                }
 #pragma unroll
-              for (int j = 0; j < H; ++j) {
-                pacc[j] = pacc[j + U];
-                xw[j] = xw[j + U];
+                for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
               }
-#pragma unroll
-              for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
-            }
+            };
+            if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           }
           release_item();
           if constexpr (H > 0) {
