@@ -63,7 +63,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   const Layout L = layout_of(p.k, p.d, es, bwd);
   p.TB = L.TB;
   p.G = (p.C + kCols - 1) / kCols;
-  p.nbk = (p.N + kConsumerWarps - 1) / kConsumerWarps;
+  p.nbk = (p.N + kBoxN - 1) / kBoxN;
   p.ttl = (p.T + p.TB - 1) / p.TB;
   const long long tpg = (long long)p.nbk * p.ttl;
   if (tpg > (1 << 30)) return false;
@@ -113,7 +113,7 @@ int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const voi
     const bool is_dy = m >= 2, halo = m & 1;
     if (is_dy && !bwd) continue;
     if (halo && p.H == 0) continue;
-    const cuuint32_t box[3] = {(cuuint32_t)kCols, (cuuint32_t)kConsumerWarps, (cuuint32_t)(halo ? p.H : p.TB)};
+    const cuuint32_t box[3] = {(cuuint32_t)kCols, (cuuint32_t)kBoxN, (cuuint32_t)(halo ? p.H : p.TB)};
     CUresult r = g_encode(&maps[m], dt, 3, const_cast<void*>(is_dy ? dy : x), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -46,11 +46,16 @@
 namespace psn {
 namespace stream {
 
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;
 constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + TMA producer warp + publisher warp
 constexpr int kCols = 32;                        // columns per tile (lanes)
+constexpr int kBoxN = kConsumerWarps;            // batch rows per tile: consumer warp w owns row w
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
-constexpr int kRowBlock = 8;                     // time rows a consumer thread advances at once (ILP)
+constexpr int kRowBlock = 4;                     // time rows a consumer thread advances at once (ILP)
+
+#ifndef PSN_TRACE_BUILD
+#define PSN_TRACE_BUILD 0  // 1: per-CTA wait/compute breakdown (PSN_TRACE=1 at run time)
+#endif
 
 #ifndef PSN_WAIT_LIMIT_NS
 #define PSN_WAIT_LIMIT_NS 4000000000ull
@@ -124,12 +129,14 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait suspends the warp in hardware (up to the hint, in ns) until the phase
+// completes, so waiting warps do not steal issue slots from working ones
 __device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
   unsigned ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(su32(b)), "r"(parity)
+      : "r"(su32(b)), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
@@ -191,14 +198,8 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 c
 }
 
 // streaming stores of the outputs (L2 evict_first: keep the resident groups)
-__device__ __forceinline__ void st_out(float* a, float v, uint64_t pol) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_out(__nv_bfloat16* a, float v, uint64_t pol) {
-  const __nv_bfloat16 b = __float2bfloat16_rn(v);
-  const unsigned short u = *reinterpret_cast<const unsigned short*>(&b);
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(a), "h"(u), "l"(pol) : "memory");
-}
+__device__ __forceinline__ void st_out(float* a, float v, uint64_t) { __stcs(a, v); }
+__device__ __forceinline__ void st_out(__nv_bfloat16* a, float v, uint64_t) { __stcs(a, __float2bfloat16_rn(v)); }
 
 // explicit shared-space loads (the stage pointers are computed from an aligned
 // integer, so the compiler would otherwise emit generic LD for them)
@@ -248,13 +249,13 @@ __device__ __forceinline__ double rcp_f64(double v) {
 struct Layout {
   int H, NV, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
 };
-__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
+__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 8 : 16) : (es == 4 ? 16 : 32); }
 __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
   L.NV = bwd ? 3 * k + 1 : 2;
   L.TB = tile_rows(es, bwd);
-  L.rowb = kConsumerWarps * kCols * es;  // bytes of one time row of a box
+  L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
   L.xbytes = xrows * L.rowb;
   L.dbytes = bwd ? xrows * L.rowb : 0;
@@ -262,7 +263,7 @@ __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
   L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
   L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
-  L.dep = kConsumerWarps * L.NV * kCols * 8;  // per-warp partial sums handed to the publisher
+  L.dep = 8 * L.NV * kCols * 8;  // per-warp-pair partial sums handed to the publisher
   L.tot = 8 * 2 * kCols * 8;                  // publisher ring: pre-update running stats of 8 groups
   L.fixed = L.dep + 4 * L.pbytes + L.tot + 512;
   return L;
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsumerWarps);
     }
-    mbar_init(depf, kConsumerWarps);
+    mbar_init(depf, 8);  // the high warp of each consumer pair arrives
     mbar_init(depe, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(p1f + i, 1);
@@ -473,13 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
         const int s = q % p.S;
         if (q >= p.S) {
-          const unsigned long long t0 = a.trace ? gtimer() : 0;
+          const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
           mbar_wait(empty + s, (unsigned)(((q / p.S) - 1) & 1));
-          if (a.trace) tr_empty += gtimer() - t0;
+          if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
         const uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
-        const int c0 = g * kCols, n0 = nbi * kConsumerWarps;
+        const int c0 = g * kCols, n0 = nbi * kBoxN;
         if (kind == kTile) {
           mbar_arrive_tx(full + s, (unsigned)(TB * C_::ROWB * (BWD ? 2 : 1)));
           tma_load3(st, &mx, c0, n0, trow, full + s, pol);
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (a.trace)
+      if (PSN_TRACE_BUILD && a.trace)
         printf("PSNTRACE %s prod cta %d total %llu empty %llu items %d\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
                gtimer() - tr_start, tr_empty, q);
     }
@@ -544,16 +545,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int v = worker_of(p, it, 0);
         if (v < p.P) {
-          const unsigned long long t0 = a.trace ? gtimer() : 0;
+          const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
           if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
           __syncwarp();
-          if (a.trace) tp_dep += gtimer() - t0;
+          if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
           double t[NV];
 #pragma unroll
           for (int val = 0; val < NV; ++val) {
             double s = dep[(0 * NV + val) * kCols + lane];
 #pragma unroll
-            for (int w2 = 1; w2 < kConsumerWarps; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
+            for (int w2 = 1; w2 < 8; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
             t[val] = s;
           }
           __syncwarp();
@@ -568,10 +569,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int g2 = it + 1 - p.lag;  // streamed by pass 2 in iteration it + 1
       if (g2 >= 0 && g2 < p.G) {
         const int sl = g2 & 1;
-        unsigned long long t0 = a.trace ? gtimer() : 0;
+        unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
         if (lane == 0) wait_counter(a.cnt + g2, (unsigned)p.nCTA, "pass-1 sums");
         __syncwarp();
-        if (a.trace) {
+        if (PSN_TRACE_BUILD && a.trace) {
           const unsigned long long t1 = gtimer();
           tp_cnt += t1 - t0;
           t0 = t1;
@@ -596,10 +597,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(p2f + sl);
-        if (a.trace) tp_fold += gtimer() - t0;
+        if (PSN_TRACE_BUILD && a.trace) tp_fold += gtimer() - t0;
       }
     }
-    if (a.trace && lane == 0)
+    if (PSN_TRACE_BUILD && a.trace && lane == 0)
       printf("PSNTRACE %s publ cta %d total %llu dep %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd",
              (int)blockIdx.x, gtimer() - tp_start, tp_dep, tp_cnt, tp_fold);
     return;
@@ -607,16 +608,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ======================= consumer warps =======================
   constexpr int U = kRowBlock;
-  constexpr int RS = kConsumerWarps * kCols;  // elements between consecutive time rows of a box
+  constexpr int RS = kBoxN * kCols;  // elements between consecutive time rows of a box
   const int n_in = warp;                      // batch row within the tile
   const uint64_t pol_out = pol_evict_first();
   int q = 0, nd = 0;
   unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
   auto wait_item = [&]() -> unsigned char* {
     const int s = q % p.S;
-    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     mbar_wait(full + s, (unsigned)((q / p.S) & 1));
-    if (a.trace) tc_full += gtimer() - t0;
+    if (PSN_TRACE_BUILD && a.trace) tc_full += gtimer() - t0;
     return smem + (size_t)s * C_::STAGE;
   };
   auto release_item = [&]() {
@@ -625,25 +626,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     ++q;
   };
   // wait for this segment's parameters; returns this lane's parameter row
-  auto take_params = [&](int g, int pass) -> const unsigned char* {
+  auto take_params = [&](int g) -> const unsigned char* {
     const int sl = g & 1;
-    const unsigned long long t0 = a.trace ? gtimer() : 0;
-    mbar_wait((pass == 0 ? p1f : p2f) + sl, (unsigned)((g >> 1) & 1));
-    if (a.trace) tc_param += gtimer() - t0;
-    return (pass == 0 ? p1s : p2s) + sl * LY.pbytes + lane * LY.pstride;
+    const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
+    mbar_wait(p2f + sl, (unsigned)((g >> 1) & 1));
+    if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
+    return p2s + sl * LY.pbytes + lane * LY.pstride;
   };
-  auto done_params = [&](int g, int pass) {
+  auto done_params = [&](int g) {
     __syncwarp();
-    if (lane == 0) mbar_arrive((pass == 0 ? p1e : p2e) + (g & 1));
+    if (lane == 0) mbar_arrive(p2e + (g & 1));
   };
+  // per-warp pass-1 sums handed to the publisher: warps w and w + 8 share slot w
+  // (the low warp stores, the high warp adds in fixed order and arrives)
   auto deposit = [&](const double* acc) {
-    const unsigned long long t0 = a.trace ? gtimer() : 0;
+    const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1));
-    if (a.trace) tc_dep += gtimer() - t0;
+    if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
+    const int sw = warp & 7;
+    if (warp < 8) {
 #pragma unroll
-    for (int val = 0; val < NV; ++val) dep[(warp * NV + val) * kCols + lane] = acc[val];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(depf);
+      for (int val = 0; val < NV; ++val) dep[(sw * NV + val) * kCols + lane] = acc[val];
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + sw) : "memory");  // pair barrier (warps sw, sw + 8)
+    if (warp >= 8) {
+#pragma unroll
+      for (int val = 0; val < NV; ++val) dep[(sw * NV + val) * kCols + lane] += acc[val];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(depf);
+    }
     ++nd;
   };
   const size_t rowstride = (size_t)p.N * p.J;
@@ -696,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int nbi = t_a / p.ttl, tt = t_a % p.ttl;
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
-          const bool lv = (unsigned)(nbi * kConsumerWarps + n_in) < mN && col < p.J;
+          const bool lv = (unsigned)(nbi * kBoxN + n_in) < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
             for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
@@ -873,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (it >= p.lag && it - p.lag < p.G) {
       const int g = it - p.lag;
       const int v = worker_of(p, g, 1);
-      const unsigned char* pr = take_params(g, 1);
+      const unsigned char* pr = take_params(g);
       const int col = g * kCols + lane;
       int t_a, t_b;
       tile_range(p, v, t_a, t_b);
@@ -886,11 +897,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
         const double bf = ldsd(pd + K);
-        done_params(g, 1);
+        done_params(g);
         int nbi = t_a / p.ttl, tt = t_a % p.ttl;
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
-          const int n = nbi * kConsumerWarps + n_in;
+          const int n = nbi * kBoxN + n_in;
           const bool lv = (unsigned)n < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
@@ -924,7 +935,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
                 const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-                if (lv && (FULL || r0 + u < nvalid)) st_out(o + (size_t)(r0 + u) * rowstride, sp, pol_out);
+                if (lv && (FULL || r0 + u < nvalid)) st_out(o, sp, pol_out);
+                o += rowstride;
               }
 #pragma unroll
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
@@ -952,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float bf = (float)ldsd(pd + K);
         const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);
-        done_params(g, 1);
+        done_params(g);
         int run_t0 = 0;
         bool lv = false;
         IO* obase = out;
@@ -1000,7 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
           if (tile == t_a || tt == 0) {
-            const int n = nbi * kConsumerWarps + n_in;
+            const int n = nbi * kBoxN + n_in;
             lv = (unsigned)n < mN && col < p.J;
             obase = out + (size_t)(lv ? n : 0) * p.J + (lv ? col : 0);
             run_t0 = t0;
@@ -1019,7 +1031,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const IO* xs = (const IO*)st + n_in * kCols + lane;
             const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
             const int nvalid = min(TB, p.T - t0);
-            const bool first = t0 == run_t0;  // rows t0-H..t0-1 of the ring belong to the previous range
             auto rows = [&](auto full_tag) {
               constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
@@ -1040,7 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                   const int od = t0 + r0 + u - H;  // complete now
-                  const bool ok = lv && (r0 + u >= H || !first) && (FULL || od < p.T);
+                  const bool ok = lv && od >= run_t0 && (FULL || od < p.T);  // rows < run_t0: previous range
                   if (ok) st_out(obase + (size_t)od * rowstride, pacc[u], pol_out);
                 }
 #pragma unroll
@@ -1077,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (a.trace && threadIdx.x == 0)
+  if (PSN_TRACE_BUILD && a.trace && threadIdx.x == 0)
     printf("PSNTRACE %s cons cta %d total %llu full %llu param %llu dep %llu items %d\n", BWD ? "bwd" : "fwd",
            (int)blockIdx.x, gtimer() - tc_start, tc_full, tc_param, tc_dep, q);
 }
