@@ -53,6 +53,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   std::call_once(g_dev_once, dev_init);
   if (!g_encode || g_sms <= 0) return false;
   const int es = (int)dtype_size(desc->dtype);
+  if (desc->T > (1 << 24) || desc->C > (1 << 24)) return false;  // group / iteration indices stay small
   p.T = (int)desc->T;
   p.N = (int)desc->N;
   p.C = (int)desc->C;
@@ -66,7 +67,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   p.nbk = (p.N + kBoxN - 1) / kBoxN;
   p.ttl = (p.T + p.TB - 1) / p.TB;
   const long long tpg = (long long)p.nbk * p.ttl;
-  if (tpg > (1 << 30)) return false;
+  if (tpg * (long long)(g_sms + 1) >= (1LL << 32)) return false;  // 32-bit schedule arithmetic
   p.tpg = (int)tpg;
   p.nCTA = g_sms;
   p.P = p.tpg < p.nCTA ? p.tpg : p.nCTA;
@@ -163,6 +164,7 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
   a.eps = desc->eps;
   a.momentum = desc->momentum;
   a.trace = env_int("PSN_TRACE", 0);
+  a.ablate = env_int("PSN_ABLATE", 0);
   return dispatch(desc, false, a, x, nullptr, st);
 }
 
@@ -189,6 +191,7 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
   a.eps = desc->eps;
   a.momentum = desc->momentum;
   a.trace = env_int("PSN_TRACE", 0);
+  a.ablate = env_int("PSN_ABLATE", 0);
   Surrogate s;
   s.kind = desc->surrogate;
   if (desc->surrogate == PSN_ARCTAN) {

@@ -38,6 +38,7 @@
 
 #include <cuda.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -47,7 +48,7 @@ namespace psn {
 namespace stream {
 
 constexpr int kConsumerWarps = 16;
-constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + TMA producer warp + publisher warp
+constexpr int kThreads = (kConsumerWarps + 3) * 32;  // + TMA producer, publisher and folder warps
 constexpr int kCols = 32;                        // columns per tile (lanes)
 constexpr int kBoxN = kConsumerWarps;            // batch rows per tile: consumer warp w owns row w
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
@@ -97,6 +98,7 @@ struct Args {
   int shared;
   double eps, momentum;
   Surrogate sur;    // f32 surrogate (dx pass)
+  int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA
   int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
   double sc, sscale; // f64 surrogate: arctan c = pi*alpha/2, scale = alpha/2; rational c = alpha, scale = 1
   int skind;
@@ -129,14 +131,12 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
-// try_wait suspends the warp in hardware (up to the hint, in ns) until the phase
-// completes, so waiting warps do not steal issue slots from working ones
 __device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
   unsigned ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(su32(b)), "r"(parity), "r"(1000000u)
+      : "r"(su32(b)), "r"(parity)
       : "memory");
   return ok != 0;
 }
@@ -146,6 +146,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   while (!mbar_try(b, parity))
     if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired("mbarrier", (int)parity, 0);
 }
+
+// keep an incrementally updated loop counter opaque, so the compiler does not
+// rematerialise it as a per-iteration integer division
+__device__ __forceinline__ void opaque(int& v) { asm volatile("" : "+r"(v)); }
 
 __device__ __forceinline__ uint64_t pol_evict_last() {
   uint64_t p;
@@ -249,7 +253,7 @@ __device__ __forceinline__ double rcp_f64(double v) {
 struct Layout {
   int H, NV, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
 };
-__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 8 : 16) : (es == 4 ? 16 : 32); }
+__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
 __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
@@ -288,13 +292,17 @@ __device__ __forceinline__ constexpr int slot(int i) {
 // -------------------------------------------------------------------------
 // static schedule, shared by the three warp roles
 // -------------------------------------------------------------------------
+// 32-bit schedule arithmetic only (a 64-bit divide is a ~100-instruction
+// subroutine, and every warp evaluates these once per segment); the planner
+// guarantees tpg * nCTA < 2^32
 __device__ __forceinline__ int worker_of(const Plan& p, int g, int pass) {
-  const int rot = (int)(((long long)g * 61 + pass * 29) % p.nCTA);
-  return ((int)blockIdx.x - rot + p.nCTA) % p.nCTA;
+  const unsigned n = (unsigned)p.nCTA;
+  const unsigned rot = ((unsigned)g * 61u + (unsigned)pass * 29u) % n;
+  return (int)(((unsigned)blockIdx.x + n - rot) % n);
 }
 __device__ __forceinline__ void tile_range(const Plan& p, int v, int& ta, int& tb) {
-  ta = (int)((long long)v * p.tpg / p.P);
-  tb = (int)((long long)(v + 1) * p.tpg / p.P);
+  ta = (int)((unsigned)v * (unsigned)p.tpg / (unsigned)p.P);
+  tb = (int)((unsigned)(v + 1) * (unsigned)p.tpg / (unsigned)p.P);
 }
 
 enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
@@ -306,11 +314,46 @@ enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
 // writes the pass-2 parameters straight into its shared-memory slot; only the
 // group's designated CTA (`store`) writes the layer outputs to global memory.
 // -------------------------------------------------------------------------
+// static per-channel inputs of a fold (loaded by the folder warp before it
+// waits for the group's sums, so their latency hides behind that wait)
 template <int K, bool BWD>
-__device__ __forceinline__ void fold_channel(const Args& a, int c, const double* tt, double rm_prev, double rv_prev,
-                                             bool store, unsigned char* prow) {
-  const Plan& p = a.p;
+struct FoldIn {
+  double W[K], gamma, beta;
+  double mu, s, aa, bf, wf[BWD ? K : 1], wq[BWD ? K : 1];  // the forward's fold row (backward only)
+};
+template <int K, bool BWD>
+__device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD>& in) {
   const double* Wc = a.W + (a.shared ? 0 : (size_t)c * K);
+#pragma unroll
+  for (int i = 0; i < K; ++i) in.W[i] = __ldg(Wc + i);
+  in.gamma = __ldg(a.gamma + c);
+  if constexpr (!BWD) {
+    in.beta = __ldg(a.beta + c);
+  } else {
+    const double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
+    in.mu = __ldg(fr + 0);
+    in.s = __ldg(fr + 1);
+    in.aa = __ldg(fr + 2);
+    in.bf = __ldg(fr + 3);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      in.wf[i] = __ldg(fr + PSN_FOLD_HDR + i);
+      in.wq[i] = __ldg(fr + PSN_FOLD_HDR + K + i);
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// fold of channel c from its per-channel pass-1 sums, one folder lane per
+// channel (forward: network.py:239-258; backward: network.py:279-317).  Every
+// CTA folds the 32 channels of the group it is about to stream in pass 2 and
+// writes the pass-2 parameters straight into its shared-memory slot; only the
+// group's designated CTA (`store`) writes the layer outputs to global memory.
+// -------------------------------------------------------------------------
+template <int K, bool BWD>
+__device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<K, BWD>& in, const double* tt,
+                                             double rm_prev, double rv_prev, bool store, unsigned char* prow) {
+  const Plan& p = a.p;
   double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
   double* pd = (double*)prow;
   const int flags = a.flags;
@@ -326,8 +369,8 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const double*
     const double mu = use_batch ? mu_b : rm_prev;  // network.py:250-255
     const double var = use_batch ? var_b : rv_prev;
     const double s = sqrt(var + a.eps);
-    const double aa = __ldg(a.gamma + c) / s;
-    const double bf = __ldg(a.beta + c) - aa * mu;
+    const double aa = in.gamma / s;
+    const double bf = in.beta - aa * mu;
     if (store) {
       if (!smooth) {  // network.py:241-248
         const double unbiased = m > 1.0 ? var_b * (m / (m - 1.0)) : var_b;
@@ -347,7 +390,7 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const double*
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      const double wf = aa * __ldg(Wc + i);
+      const double wf = aa * in.W[i];
       double wq = wf;
       if (quantize) {  // quant.py:111-139
         int sg, e;
@@ -363,7 +406,7 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const double*
     pd[K] = bf;
   } else {
     float* pf = (float*)(prow + 8 * (K + 1));
-    const double mu = __ldg(fr + 0), s = __ldg(fr + 1), aa = __ldg(fr + 2);
+    const double mu = in.mu, s = in.s, aa = in.aa;
     const bool quantized = (flags & PSN_QUANTIZED) && (!(flags & PSN_SMOOTH) || (flags & PSN_QUANTIZE_IN_SMOOTH));
     const double db_f = tt[0] * a.sscale;
     double da = 0.0, dwf[K];
@@ -371,16 +414,16 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const double*
     for (int i = 0; i < K; ++i) {  // quantize_backward, quant.py:194-216
       double g1 = tt[1 + i] * a.sscale;
       if (quantized && (flags & PSN_ROUND_STE)) {
-        const double wf = __ldg(fr + PSN_FOLD_HDR + i), wq = __ldg(fr + PSN_FOLD_HDR + K + i);
+        const double wf = in.wf[i], wq = in.wq[i];
         g1 = (wf != 0.0) ? g1 * (fabs(wq) / fabs(wf)) : 0.0;
       }
       dwf[i] = g1;
-      da = da + dwf[i] * __ldg(Wc + i);
+      da = da + dwf[i] * in.W[i];
     }
     da = da - db_f * mu;  // network.py:291-296
     double alpha1 = 0.0, beta1 = 0.0;
     if (flags & PSN_USE_BATCH_STATS) {  // network.py:298-315
-      const double ds = -da * __ldg(a.gamma + c) / (s * s);
+      const double ds = -da * in.gamma / (s * s);
       const double dvar = ds / (2.0 * s);
       const double dmu = -db_f * aa;
       alpha1 = dmu / m;
@@ -398,17 +441,17 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const double*
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      pd[i] = __ldg(fr + PSN_FOLD_HDR + K + i);  // w_q
-      pf[i] = (float)__ldg(Wc + i);
+      pd[i] = in.wq[i];
+      pf[i] = (float)in.W[i];
     }
-    pd[K] = __ldg(fr + 3);  // b_f
+    pd[K] = in.bf;
     pf[K] = (float)mu;
     pf[K + 1] = (float)alpha1;
     pf[K + 2] = (float)beta1;
   }
 }
 
-__device__ __forceinline__ int designated_of(const Plan& p, int g) { return (int)(((long long)g * 37 + 11) % p.nCTA); }
+__device__ __forceinline__ int designated_of(const Plan& p, int g) { return (int)(((unsigned)g * 37u + 11u) % (unsigned)p.nCTA); }
 
 __device__ __forceinline__ void red_add_f64(double* a, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
@@ -470,18 +513,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (BWD && H > 0) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&myh) : "memory");
       const uint64_t pol_keep = pol_evict_last(), pol_drop = pol_evict_first(), pol_norm = pol_evict_normal();
       unsigned long long tr_start = gtimer(), tr_empty = 0;
-      int q = 0;
+      int q = 0, s = 0;
+      unsigned ph = 0;  // parity of the current pass over the ring
       auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
-        const int s = q % p.S;
         if (q >= p.S) {
           const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-          mbar_wait(empty + s, (unsigned)(((q / p.S) - 1) & 1));
+          mbar_wait(empty + s, ph ^ 1u);
           if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
         const uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
         const int c0 = g * kCols, n0 = nbi * kBoxN;
-        if (kind == kTile) {
+        if (a.ablate & 4) {
+          mbar_arrive(full + s);
+        } else if (kind == kTile) {
           mbar_arrive_tx(full + s, (unsigned)(TB * C_::ROWB * (BWD ? 2 : 1)));
           tma_load3(st, &mx, c0, n0, trow, full + s, pol);
           if (BWD) tma_load3(st + C_::XBYTES, &my, c0, n0, trow, full + s, pol);
@@ -494,6 +539,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load3(st + C_::XBYTES, &myh, c0, n0, trow, full + s, pol);
         }
         ++q;
+        if (++s == p.S) {
+          s = 0;
+          ph ^= 1u;
+        }
       };
       for (int it = 0; it < iters; ++it) {
         for (int pass = 0; pass < 2; ++pass) {
@@ -513,6 +562,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tt = 0;
               ++nbi;
             }
+            opaque(tt);
+            opaque(nbi);
           }
         }
       }
@@ -523,86 +574,101 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
+  double* prev = tot;  // [8][2][32] ring: pre-update running mean / var per group (forward only)
   if (warp == kConsumerWarps + 1) {
     // ======================= publisher warp =======================
-    // per iteration it: (1) hand this CTA's pass-1 sums of group `it` to the
-    // grid (CTA reduction over the 8 batch-row warps in fixed order, then f64
-    // atomic adds into the group's per-channel accumulators) and arrive on the
-    // group counter -- every CTA arrives, workers or not, after reading the
-    // pre-update running statistics it will fold with; (2) for the group pass 2
-    // streams next iteration: wait until every CTA arrived, fold the 32 channels
-    // (lane = channel) into the pass-2 parameter slot.
-    unsigned long long tp_start = gtimer(), tp_dep = 0, tp_cnt = 0, tp_fold = 0;
+    // per group `it`: snapshot the pre-update running statistics the fold will
+    // use (prefetched one group ahead), hand this CTA's pass-1 sums to the grid
+    // (fixed-order reduction over the consumer-pair slots, then f64 atomic adds
+    // into the group's per-channel accumulators) and arrive on the group
+    // counter -- every CTA arrives, workers or not.
+    unsigned long long tp_start = gtimer(), tp_dep = 0;
     int nd = 0;
-    double* prev = tot;  // [8][2][32] ring: running mean / var (pre-update) per group, forward only
-    for (int it = 0; it < iters; ++it) {
-      if (it < p.G) {
-        const int c = it * kCols + lane;
-        if (!BWD) {
-          const bool cv = c < p.C;
-          prev[((it & 7) * 2 + 0) * kCols + lane] = cv ? __ldcg(a.rm + c) : 0.0;
-          prev[((it & 7) * 2 + 1) * kCols + lane] = cv ? __ldcg(a.rv + c) : 0.0;
-        }
-        const int v = worker_of(p, it, 0);
-        if (v < p.P) {
-          const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-          if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
-          __syncwarp();
-          if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
-          double t[NV];
-#pragma unroll
-          for (int val = 0; val < NV; ++val) {
-            double s = dep[(0 * NV + val) * kCols + lane];
-#pragma unroll
-            for (int w2 = 1; w2 < 8; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
-            t[val] = s;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(depe);
-#pragma unroll
-          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
-          ++nd;
-        }
-        __syncwarp();
-        if (lane == 0) red_release(a.cnt + it, 1u);
+    double nrm = 0.0, nrv = 0.0;
+    auto prefetch_stats = [&](int g) {
+      const int c = g * kCols + lane;
+      nrm = c < p.C ? __ldcg(a.rm + c) : 0.0;
+      nrv = c < p.C ? __ldcg(a.rv + c) : 0.0;
+    };
+    if (!BWD && p.G > 0) prefetch_stats(0);
+    for (int it = 0; it < p.G; ++it) {
+      if (!BWD) {
+        prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
+        prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
+        if (it + 1 < p.G) prefetch_stats(it + 1);
       }
-      const int g2 = it + 1 - p.lag;  // streamed by pass 2 in iteration it + 1
-      if (g2 >= 0 && g2 < p.G) {
-        const int sl = g2 & 1;
-        unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-        if (lane == 0) wait_counter(a.cnt + g2, (unsigned)p.nCTA, "pass-1 sums");
+      const int v = worker_of(p, it, 0);
+      if (v < p.P) {
+        const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
+        if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
         __syncwarp();
-        if (PSN_TRACE_BUILD && a.trace) {
-          const unsigned long long t1 = gtimer();
-          tp_cnt += t1 - t0;
-          t0 = t1;
-        }
-        if (g2 >= 2) {
-          if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((g2 >> 1) - 1) & 1));
-          __syncwarp();
-        }
-        const int c = g2 * kCols + lane;
-        if (c < p.C) {
-          double tt[NV];
+        if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
+        double t[NV];
 #pragma unroll
-          for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g2 * NV + val) * kCols + lane);
-          const double rmp = BWD ? 0.0 : prev[((g2 & 7) * 2 + 0) * kCols + lane];
-          const double rvp = BWD ? 0.0 : prev[((g2 & 7) * 2 + 1) * kCols + lane];
-          fold_channel<K, BWD>(a, c, tt, rmp, rvp, designated_of(p, g2) == (int)blockIdx.x,
-                               p2s + sl * LY.pbytes + lane * LY.pstride);
-        } else {
-          double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
+        for (int val = 0; val < NV; ++val) {
+          double s = dep[(0 * NV + val) * kCols + lane];
 #pragma unroll
-          for (int i = 0; i < LY.pstride / 8; ++i) pd[i] = 0.0;
+          for (int w2 = 1; w2 < 8; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
+          t[val] = s;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(p2f + sl);
-        if (PSN_TRACE_BUILD && a.trace) tp_fold += gtimer() - t0;
+        if (lane == 0) mbar_arrive(depe);
+#pragma unroll
+        for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
+        ++nd;
       }
+      __syncwarp();
+      if (lane == 0) red_release(a.cnt + it, 1u);
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
-      printf("PSNTRACE %s publ cta %d total %llu dep %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd",
-             (int)blockIdx.x, gtimer() - tp_start, tp_dep, tp_cnt, tp_fold);
+      printf("PSNTRACE %s publ cta %d total %llu dep %llu\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
+             gtimer() - tp_start, tp_dep);
+    return;
+  }
+
+  if (warp == kConsumerWarps + 2) {
+    // ======================= folder warp =======================
+    // per group g, in order: load the static fold inputs, wait until every CTA
+    // arrived on the group counter, fold the group's 32 channels (lane =
+    // channel) into the pass-2 parameter slot the consumers read.
+    unsigned long long tf_start = gtimer(), tf_cnt = 0, tf_fold = 0;
+    for (int g = 0; g < p.G; ++g) {
+      const int sl = g & 1;
+      const int c = g * kCols + lane;
+      FoldIn<K, BWD> in;
+      if (c < p.C) load_fold_in<K, BWD>(a, c, in);
+      unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
+      if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)p.nCTA, "pass-1 sums");
+      __syncwarp();
+      if (PSN_TRACE_BUILD && a.trace) {
+        const unsigned long long t1 = gtimer();
+        tf_cnt += t1 - t0;
+        t0 = t1;
+      }
+      if (g >= 2) {
+        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((g >> 1) - 1) & 1));
+        __syncwarp();
+      }
+      if (c < p.C) {
+        double tt[NV];
+#pragma unroll
+        for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
+        const double rmp = BWD ? 0.0 : prev[((g & 7) * 2 + 0) * kCols + lane];
+        const double rvp = BWD ? 0.0 : prev[((g & 7) * 2 + 1) * kCols + lane];
+        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, designated_of(p, g) == (int)blockIdx.x,
+                             p2s + sl * LY.pbytes + lane * LY.pstride);
+      } else {
+        double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
+#pragma unroll
+        for (int i = 0; i < LY.pstride / 8; ++i) pd[i] = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p2f + sl);
+      if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
+    }
+    if (PSN_TRACE_BUILD && a.trace && lane == 0)
+      printf("PSNTRACE %s fold cta %d total %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
+             gtimer() - tf_start, tf_cnt, tf_fold);
     return;
   }
 
@@ -611,21 +677,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int RS = kBoxN * kCols;  // elements between consecutive time rows of a box
   const int n_in = warp;                      // batch row within the tile
   const uint64_t pol_out = pol_evict_first();
-  int q = 0, nd = 0;
+  int q = 0, nd = 0, cs = 0;
+  unsigned cph = 0;  // parity of the current pass over the ring
   unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
   auto wait_item = [&]() -> unsigned char* {
-    const int s = q % p.S;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait(full + s, (unsigned)((q / p.S) & 1));
+    mbar_wait(full + cs, cph);
     if (PSN_TRACE_BUILD && a.trace) tc_full += gtimer() - t0;
-    return smem + (size_t)s * C_::STAGE;
+    return smem + (size_t)cs * C_::STAGE;
   };
   auto release_item = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + (q % p.S));
+    if (lane == 0) mbar_arrive(empty + cs);
     ++q;
+    if (++cs == p.S) {
+      cs = 0;
+      cph ^= 1u;
+    }
   };
-  // wait for this segment's parameters; returns this lane's parameter row
   auto take_params = [&](int g) -> const unsigned char* {
     const int sl = g & 1;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
@@ -750,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
           };
-          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           if (!lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
 #pragma unroll
             for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
@@ -765,6 +834,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tt = 0;
             ++nbi;
           }
+          opaque(tt);
+          opaque(nbi);
         }
       } else {
         // ---- backward pass 1: db, dw_q (f64 end to end: h2 exact and f32-rounded like the
@@ -866,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
-          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             acc[1 + K + i] += (double)fsx[i];
@@ -874,6 +945,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           release_item();
           if (++tt == p.ttl) tt = 0;
+          opaque(tt);
         }
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
@@ -942,12 +1014,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
           };
-          if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
           }
+          opaque(tt);
+          opaque(nbi);
         }
       } else {
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
@@ -1063,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
               }
             };
-            if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+            if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           }
           release_item();
           if constexpr (H > 0) {
@@ -1084,6 +1158,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tt = 0;
             ++nbi;
           }
+          opaque(tt);
+          opaque(nbi);
         }
       }
     }
