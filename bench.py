@@ -246,11 +246,20 @@ def main():
     hbm, peak_src = _peaks()
     f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
     fwd_bytes, bwd_bytes = 2 * esize * nel, 3 * esize * nel
-    fname = "fused_fwd_kernel" if plan_f.get("fused") else "psn_forward_train (3 kernels)"
-    bname = "fused_bwd_kernel" if plan_b.get("fused") else "psn_backward (3 kernels)"
+    fname = "psn_stream_kernel<fwd>" if plan_f.get("streamed") else "psn_forward_train (3 generic kernels)"
+    bname = "psn_stream_kernel<bwd>" if plan_b.get("streamed") else "psn_backward (3 generic kernels)"
     groups = {fname: (fwd_bytes, f_ms), bname: (bwd_bytes, b_ms)}
     dom_name, (dom_bytes, dom_ms) = max(groups.items(), key=lambda kv: kv[1][1])
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None  # dram read+write bytes per launch of the dominant kernel, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        key = next((kk for kk in tr if (("1>" in kk) == ("bwd" in dom_name)) and f"<{k}, {d}, float" in kk), None)
+        if key is not None and args.dtype == "f32" and (T, B, C) == (1024, 64, 512):
+            traffic = tr[key]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
     step_achieved = (5 * esize * nel) / ((f_ms + b_ms) * 1e-3) / 1e9
 
     # ---- e2e through the public module API with host buffers -----------------
@@ -313,7 +322,7 @@ def main():
                        "T": T, "B_per_gpu": B, "C": C, "k": k, "d": d, "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (x, dy each %.0f MB > 126 MB L2)" % (nel * esize / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "kernel": dom_name,
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": dom_name,
                          "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
                          "peak_source": peak_src},
             "step_roofline": {"achieved": step_achieved, "frac": step_achieved / hbm,

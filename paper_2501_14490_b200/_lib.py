@@ -145,7 +145,7 @@ def workspace(desc: PsnDesc, device) -> torch.Tensor:
 def plan_info(desc: PsnDesc, backward: bool) -> dict:
     buf = (ctypes.c_int64 * 6)()
     n = lib().psn_plan_info(ctypes.byref(desc), int(backward), buf, 6)
-    keys = ("fused", "ctas", "groups", "tiles_per_group", "row_slices", "launches")
+    keys = ("streamed", "ctas", "groups", "tiles_per_group", "stages", "launches")
     return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
 
 

@@ -140,11 +140,16 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
       : "memory");
   return ok != 0;
 }
+// waiting warps back off with nanosleep so they do not steal issue slots from
+// the warps doing arithmetic (latency-tolerant roles sleep longer)
+template <unsigned SLEEP_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   if (mbar_try(b, parity)) return;
   const unsigned long long t0 = gtimer();
-  while (!mbar_try(b, parity))
+  while (!mbar_try(b, parity)) {
+    if (SLEEP_NS) __nanosleep(SLEEP_NS);
     if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired("mbarrier", (int)parity, 0);
+  }
 }
 
 // keep an incrementally updated loop counter opaque, so the compiler does not
@@ -192,7 +197,7 @@ __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target,
   const unsigned long long t0 = gtimer();
   unsigned v;
   while ((v = ld_acquire(a)) < target) {
-    __nanosleep(64);
+    __nanosleep(256);
     if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired(what, (int)v, (int)target);
   }
 }
@@ -518,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
         if (q >= p.S) {
           const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-          mbar_wait(empty + s, ph ^ 1u);
+          mbar_wait<128>(empty + s, ph ^ 1u);
           if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int v = worker_of(p, it, 0);
       if (v < p.P) {
         const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-        if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
+        if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
         __syncwarp();
         if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
         double t[NV];
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         t0 = t1;
       }
       if (g >= 2) {
-        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((g >> 1) - 1) & 1));
+        if (lane == 0) mbar_wait<256>(p2e + sl, (unsigned)(((g >> 1) - 1) & 1));
         __syncwarp();
       }
       if (c < p.C) {
@@ -682,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
   auto wait_item = [&]() -> unsigned char* {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait(full + cs, cph);
+    mbar_wait<32>(full + cs, cph);
     if (PSN_TRACE_BUILD && a.trace) tc_full += gtimer() - t0;
     return smem + (size_t)cs * C_::STAGE;
   };
@@ -698,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto take_params = [&](int g) -> const unsigned char* {
     const int sl = g & 1;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait(p2f + sl, (unsigned)((g >> 1) & 1));
+    mbar_wait<64>(p2f + sl, (unsigned)((g >> 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
     return p2s + sl * LY.pbytes + lane * LY.pstride;
   };
@@ -710,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (the low warp stores, the high warp adds in fixed order and arrives)
   auto deposit = [&](const double* acc) {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1));
+    if (nd >= 1) mbar_wait<64>(depe, (unsigned)((nd - 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
     const int sw = warp & 7;
     if (warp < 8) {
