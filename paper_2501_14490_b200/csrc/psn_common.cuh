@@ -146,12 +146,14 @@ struct Surrogate {
   float scale;    // arctan: alpha/2    ; rational: 1
 };
 
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 __device__ __forceinline__ float surrogate_grad(const Surrogate& s, float h) {
-  if (s.kind == PSN_ARCTAN) {
-    const float u = s.c * h;
-    return __fdividef(s.scale, fmaf(u, u, 1.0f));
-  }
-  return __fdividef(1.0f, fmaf(s.c * h, h, 1.0f));
+  const float t = s.c * h;
+  return s.scale * rcp_approx(fmaf(t, s.kind == PSN_ARCTAN ? t : h, 1.0f));
 }
 
 // spike_primitive (surrogate.py:42-54) in f64 for SMOOTH mode

@@ -54,6 +54,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   if (!g_encode || g_sms <= 0) return false;
   const int es = (int)dtype_size(desc->dtype);
   if (desc->T > (1 << 24) || desc->C > (1 << 24)) return false;  // group / iteration indices stay small
+  if ((double)desc->T * desc->N * desc->C >= 4294967296.0) return false;  // 32-bit element offsets
   p.T = (int)desc->T;
   p.N = (int)desc->N;
   p.C = (int)desc->C;

@@ -197,7 +197,7 @@ __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target,
   const unsigned long long t0 = gtimer();
   unsigned v;
   while ((v = ld_acquire(a)) < target) {
-    __nanosleep(256);
+    __nanosleep(1000);
     if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired(what, (int)v, (int)target);
   }
 }
@@ -210,6 +210,22 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 c
 __device__ __forceinline__ void st_out(float* a, float v, uint64_t) { __stcs(a, v); }
 __device__ __forceinline__ void st_out(__nv_bfloat16* a, float v, uint64_t) { __stcs(a, __float2bfloat16_rn(v)); }
 
+// shared-space loads from 32-bit shared-window addresses (no generic pointer,
+// no per-load address-space conversion)
+template <typename IO>
+__device__ __forceinline__ float ldsx(uint32_t a);
+template <>
+__device__ __forceinline__ float ldsx<float>(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ float ldsx<__nv_bfloat16>(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return __uint_as_float(((unsigned)v) << 16);
+}
 // explicit shared-space loads (the stage pointers are computed from an aligned
 // integer, so the compiler would otherwise emit generic LD for them)
 __device__ __forceinline__ float lds(const float* p) {
@@ -557,7 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (v >= p.P) continue;
           int t_a, t_b;
           tile_range(p, v, t_a, t_b);
-          int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+          int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        opaque(nbi);
+        opaque(tt);
           for (int tile = t_a; tile < t_b; ++tile) {
             const int t0 = tt * TB;
             if (H > 0 && tile == t_a && t0 > 0) issue(kHead, pass, g, nbi, t0 - H);
@@ -680,16 +698,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ======================= consumer warps =======================
   constexpr int U = kRowBlock;
   constexpr int RS = kBoxN * kCols;  // elements between consecutive time rows of a box
+  constexpr uint32_t RSB = RS * sizeof(IO);  // ... in bytes
   const int n_in = warp;                      // batch row within the tile
   const uint64_t pol_out = pol_evict_first();
   int q = 0, nd = 0, cs = 0;
   unsigned cph = 0;  // parity of the current pass over the ring
   unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
-  auto wait_item = [&]() -> unsigned char* {
+  const uint32_t sbase = su32(smem) + (uint32_t)((n_in * kCols + lane) * sizeof(IO));  // this thread's column
+  auto wait_item = [&]() -> uint32_t {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     mbar_wait<32>(full + cs, cph);
     if (PSN_TRACE_BUILD && a.trace) tc_full += gtimer() - t0;
-    return smem + (size_t)cs * C_::STAGE;
+    return sbase + (uint32_t)(cs * C_::STAGE);
   };
   auto release_item = [&]() {
     __syncwarp();
@@ -732,6 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ++nd;
   };
   const size_t rowstride = (size_t)p.N * p.J;
+  const uint32_t rs32 = (uint32_t)rowstride;  // the planner guarantees T*N*C < 2^32
   const unsigned mN = (unsigned)p.N;
   // pass-1 parameters are inputs of this launch (W, running mean / the forward's
   // fold rows), so each consumer loads its column's next segment one segment ahead
@@ -778,7 +799,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < K; ++i) w[i] = np1d[i];
         sh = np1d[K];
         if (g + 1 < p.G) prefetch_p1(g + 1);
-        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        opaque(nbi);
+        opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
           const bool lv = (unsigned)(nbi * kBoxN + n_in) < mN && col < p.J;
@@ -787,14 +810,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-            const unsigned char* st = wait_item();
-            const IO* xs = (const IO*)st + n_in * kCols + lane;
+            const uint32_t st = wait_item();
+            const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)lds(xs + r * RS);
+            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
-          const unsigned char* st = wait_item();
-          const IO* xs = (const IO*)st + n_in * kCols + lane;
+          const uint32_t st = wait_item();
+          const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
           double S1[U], S2[U];
 #pragma unroll
@@ -805,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
               double h[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
@@ -861,6 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mu = np1f[K];
         if (g + 1 < p.G) prefetch_p1(g + 1);
         int tt = t_a % p.ttl;
+        opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
           if (tile == t_a || tt == 0) {
@@ -871,18 +895,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-            const unsigned char* st = wait_item();
-            const IO* xs = (const IO*)st + n_in * kCols + lane;
+            const uint32_t st = wait_item();
+            const uint32_t xs = st;
 #pragma unroll
             for (int r = 0; r < H; ++r) {
-              xw[r] = lds(xs + r * RS);
+              xw[r] = ldsx<IO>(xs + (r) * RSB);
               xd[r] = (double)xw[r];
             }
             release_item();
           }
-          const unsigned char* st = wait_item();
-          const IO* xs = (const IO*)st + n_in * kCols + lane;
-          const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
+          const uint32_t st = wait_item();
+          const uint32_t xs = st;
+          const uint32_t ys = st + C_::XBYTES;
           const int nvalid = min(TB, p.T - t0);
           float fsx[K], fsc[K];
 #pragma unroll
@@ -894,9 +918,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               double yv[U], h2[U], dh[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                xw[H + u] = lds(xs + (r0 + u) * RS);
+                xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
                 xd[H + u] = (double)xw[H + u];
-                yv[u] = (double)lds(ys + (r0 + u) * RS);  // rows >= T: TMA zero fill -> dh2 = 0
+                yv[u] = (double)ldsx<IO>(ys + ((r0 + u)) * RSB);  // rows >= T: TMA zero fill -> dh2 = 0
               }
 #pragma unroll
               for (int u = 0; u < U; ++u) h2[u] = wq[0] * xd[u + slot<K, D>(0)];  // exact products
@@ -975,7 +999,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
         const double bf = ldsd(pd + K);
         done_params(g);
-        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        opaque(nbi);
+        opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
           const int n = nbi * kBoxN + n_in;
@@ -985,22 +1011,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-            const unsigned char* st = wait_item();
-            const IO* xs = (const IO*)st + n_in * kCols + lane;
+            const uint32_t st = wait_item();
+            const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)lds(xs + r * RS);
+            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
-          const unsigned char* st = wait_item();
-          const IO* xs = (const IO*)st + n_in * kCols + lane;
+          const uint32_t st = wait_item();
+          const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
-          IO* o = out + ((size_t)t0 * mN + (lv ? n : 0)) * p.J + (lv ? col : 0);
+          uint32_t ooff = ((uint32_t)t0 * mN + (uint32_t)(lv ? n : 0)) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)lds(xs + (r0 + u) * RS);
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
               double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
@@ -1012,8 +1038,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
                 const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-                if (lv && (FULL || r0 + u < nvalid)) st_out(o, sp, pol_out);
-                o += rowstride;
+                if (lv && (FULL || r0 + u < nvalid)) st_out(out + ooff, sp, pol_out);
+                ooff += rs32;
               }
 #pragma unroll
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
@@ -1046,9 +1072,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         done_params(g);
         int run_t0 = 0;
         bool lv = false;
-        IO* obase = out;
+        uint32_t obase = 0;
         auto emit = [&](int od, float val) {
-          if (lv && od >= run_t0 && od < p.T) st_out(obase + (size_t)od * rowstride, val, pol_out);
+          if (lv && od >= run_t0 && od < p.T) st_out(out + (obase + (uint32_t)od * rs32), val, pol_out);
         };
         auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1) {
           float h1 = w[0] * xw[u + slot<K, D>(0)], h2 = wq[0] * xw[u + slot<K, D>(0)];
@@ -1087,28 +1113,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             pacc[H + U - 1] = 0.f;
           }
         };
-        int nbi = t_a / p.ttl, tt = t_a % p.ttl;
+        int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        opaque(nbi);
+        opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
           if (tile == t_a || tt == 0) {
             const int n = nbi * kBoxN + n_in;
             lv = (unsigned)n < mN && col < p.J;
-            obase = out + (size_t)(lv ? n : 0) * p.J + (lv ? col : 0);
+            obase = (uint32_t)(lv ? n : 0) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
             run_t0 = t0;
 #pragma unroll
             for (int j = 0; j < H + U; ++j) xw[j] = pacc[j] = 0.f;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
-            const unsigned char* st = wait_item();
-            const IO* xs = (const IO*)st + n_in * kCols + lane;
+            const uint32_t st = wait_item();
+            const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = lds(xs + r * RS);
+            for (int r = 0; r < H; ++r) xw[r] = ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
-          const unsigned char* st = wait_item();
+          const uint32_t st = wait_item();
           {
-            const IO* xs = (const IO*)st + n_in * kCols + lane;
-            const IO* ys = (const IO*)(st + C_::XBYTES) + n_in * kCols + lane;
+            const uint32_t xs = st;
+            const uint32_t ys = st + C_::XBYTES;
             const int nvalid = min(TB, p.T - t0);
             auto rows = [&](auto full_tag) {
               constexpr bool FULL = decltype(full_tag)::value;
@@ -1116,10 +1144,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int r0 = 0; r0 < TB; r0 += U) {
                 float dh2[U], dh1[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) xw[H + u] = lds(xs + (r0 + u) * RS);
+                for (int u = 0; u < U; ++u) xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                  dh_row(u, lds(ys + (r0 + u) * RS), FULL || r0 + u < nvalid, dh2[u], dh1[u]);
+                  dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u]);
 #pragma unroll
                 for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -1131,7 +1159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u) {
                   const int od = t0 + r0 + u - H;  // complete now
                   const bool ok = lv && od >= run_t0 && (FULL || od < p.T);  // rows < run_t0: previous range
-                  if (ok) st_out(obase + (size_t)od * rowstride, pacc[u], pol_out);
+                  if (ok) st_out(out + (obase + (uint32_t)od * rs32), pacc[u], pol_out);
                 }
 #pragma unroll
                 for (int j = 0; j < H; ++j) {
@@ -1149,13 +1177,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t0 + TB >= p.T) {
               drain(t0 + TB);
             } else if (tile == t_b - 1) {  // range ends mid-stream: future dh from the TAIL rows
-              const unsigned char* st2 = wait_item();
-              const IO* xs = (const IO*)st2 + n_in * kCols + lane;
-              const IO* ys = (const IO*)(st2 + C_::XBYTES) + n_in * kCols + lane;
+              const uint32_t st2 = wait_item();
+              const uint32_t xs = st2;
+              const uint32_t ys = st2 + C_::XBYTES;
               const int te = t0 + TB;
               const int nvalid = min(H, p.T - te);
 #pragma unroll
-              for (int r = 0; r < H; ++r) step1(lds(xs + r * RS), lds(ys + r * RS), r < nvalid, te + r);
+              for (int r = 0; r < H; ++r) step1(ldsx<IO>(xs + (r) * RSB), ldsx<IO>(ys + (r) * RSB), r < nvalid, te + r);
               release_item();
             }
           }
