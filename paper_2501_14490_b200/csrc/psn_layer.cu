@@ -95,7 +95,7 @@ WsLayout ws_layout(const psn_desc_t* desc) {
   w.dwtmp = off;
   off = align256(off + sizeof(double) * (size_t)g.k * g.C);
   w.evalfold = off;
-  off = align256(off + sizeof(double) * (PSN_FOLD_HDR + 2 * (size_t)g.k) * g.C);
+  off = align256(off + sizeof(double) * PSN_FOLD_STRIDE((size_t)g.k) * g.C);
   w.fused = off;
   off = align256(off + stream::workspace_bytes(desc));
   w.total = off;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) fwd_fold_kernel(Geom g, const double
   const double a = gamma[c] / s;
   const double b_f = beta[c] - a * mu;
   const double* Wc = W + ((flags & PSN_SHARED) ? 0 : c * K);
-  double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  double* f = fold + c * PSN_FOLD_STRIDE(K);
   f[0] = mu;
   f[1] = s;
   f[2] = a;
@@ -328,7 +328,7 @@ __global__ void eval_fold_kernel(Geom g, const double* __restrict__ W, int flags
   const double scale = gamma[c] / sqrt(running_var[c] + eps);
   const double b_f = beta[c] - scale * running_mean[c];
   const double* Wc = W + ((flags & PSN_SHARED) ? 0 : c * K);
-  double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  double* f = fold + c * PSN_FOLD_STRIDE(K);
   f[0] = running_mean[c];
   f[1] = 0.0;
   f[2] = scale;
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) fwd_spike_kernel(Geom g, const IO* _
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const bool jv = j < g.J;
   const int64_t c = jv ? j / g.Q : 0;
-  const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  const double* f = fold + c * PSN_FOLD_STRIDE(K);
   double wq[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) wq[i] = jv ? f[PSN_FOLD_HDR + K + i] : 0.0;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const bool jv = j < g.J;
   const int64_t c = jv ? j / g.Q : 0;
-  const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  const double* f = fold + c * PSN_FOLD_STRIDE(K);
   double w[K], wq[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kThreads) bwd_fold_kernel(Geom g, const double
     tot[v] = acc;
   }
   if (lane != 0) return;
-  const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  const double* f = fold + c * PSN_FOLD_STRIDE(K);
   const double mu = f[0], s = f[1], a = f[2];
   const bool quantized = (flags & PSN_QUANTIZED) &&
                          (!(flags & PSN_SMOOTH) || (flags & PSN_QUANTIZE_IN_SMOOTH));
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const bool jv = j < g.J;
   const int64_t c = jv ? j / g.Q : 0;
-  const double* f = fold + c * (PSN_FOLD_HDR + 2 * K);
+  const double* f = fold + c * PSN_FOLD_STRIDE(K);
   double w[K], wq[K];
   Acc wa[K], wqa[K];
 #pragma unroll
@@ -776,7 +776,7 @@ int psn_max_order(void) { return PSN_MAX_ORDER; }
 
 size_t psn_fold_doubles(const psn_desc_t* desc) {
   if (!desc) return 0;
-  return (size_t)desc->C * (PSN_FOLD_HDR + 2 * (size_t)desc->k);
+  return (size_t)desc->C * PSN_FOLD_STRIDE((size_t)desc->k);
 }
 
 size_t psn_workspace_bytes(const psn_desc_t* desc) {

@@ -89,7 +89,7 @@ static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // workspace: group counters | per-channel f64 sums (both zeroed per launch)
 static size_t zeroed_bytes(const Plan& p, bool bwd) {
-  const size_t nv = bwd ? 3 * (size_t)p.k + 1 : 2;
+  const size_t nv = bwd ? 1 + (size_t)p.k : 2 + 2 * (size_t)p.k;
   return a256(sizeof(unsigned) * p.G) + sizeof(double) * p.G * nv * kCols;
 }
 

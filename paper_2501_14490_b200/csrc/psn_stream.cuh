@@ -54,6 +54,13 @@ constexpr int kBoxN = kConsumerWarps;            // batch rows per tile: consume
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
 constexpr int kRowBlock = 4;                     // time rows a consumer thread advances at once (ILP)
 
+#ifndef PSN_TB_FWD
+#define PSN_TB_FWD 32  // f32 time rows per forward tile (bf16: twice)
+#endif
+#ifndef PSN_TB_BWD
+#define PSN_TB_BWD 16  // f32 time rows per backward tile (x + dy)
+#endif
+
 #ifndef PSN_TRACE_BUILD
 #define PSN_TRACE_BUILD 0  // 1: per-CTA wait/compute breakdown (PSN_TRACE=1 at run time)
 #endif
@@ -88,7 +95,7 @@ struct Args {
   const double* beta;
   double* rm;             // running mean / var (forward, updated by the fold)
   double* rv;
-  double* fold;           // [C][PSN_FOLD_HDR + 2k] (written by forward, read by backward)
+  double* fold;           // [C][PSN_FOLD_STRIDE(k)] (written by forward, read by backward)
   double* dW;             // [C,k] (or per-channel scratch when shared)
   double* dgamma;
   double* dbeta;
@@ -274,11 +281,11 @@ __device__ __forceinline__ double rcp_f64(double v) {
 struct Layout {
   int H, NV, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
 };
-__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? 16 : 32) : (es == 4 ? 32 : 64); }
+__host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? PSN_TB_BWD : 2 * PSN_TB_BWD) : (es == 4 ? PSN_TB_FWD : 2 * PSN_TB_FWD); }
 __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
-  L.NV = bwd ? 3 * k + 1 : 2;
+  L.NV = bwd ? 1 + k : 2 + 2 * k;  // fwd: S1, S2, sx[k], sxh[k]; bwd: db, dw_q[k]
   L.TB = tile_rows(es, bwd);
   L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
@@ -341,6 +348,7 @@ template <int K, bool BWD>
 struct FoldIn {
   double W[K], gamma, beta;
   double mu, s, aa, bf, wf[BWD ? K : 1], wq[BWD ? K : 1];  // the forward's fold row (backward only)
+  double sx[BWD ? K : 1], sxh[BWD ? K : 1];                 // BN-term sums cached by the forward
 };
 template <int K, bool BWD>
 __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD>& in) {
@@ -351,7 +359,7 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
   if constexpr (!BWD) {
     in.beta = __ldg(a.beta + c);
   } else {
-    const double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
+    const double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
     in.mu = __ldg(fr + 0);
     in.s = __ldg(fr + 1);
     in.aa = __ldg(fr + 2);
@@ -360,6 +368,8 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
     for (int i = 0; i < K; ++i) {
       in.wf[i] = __ldg(fr + PSN_FOLD_HDR + i);
       in.wq[i] = __ldg(fr + PSN_FOLD_HDR + K + i);
+      in.sx[i] = __ldg(fr + PSN_FOLD_HDR + 2 * K + i);
+      in.sxh[i] = __ldg(fr + PSN_FOLD_HDR + 3 * K + i);
     }
   }
 }
@@ -375,7 +385,7 @@ template <int K, bool BWD>
 __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<K, BWD>& in, const double* tt,
                                              double rm_prev, double rv_prev, bool store, unsigned char* prow) {
   const Plan& p = a.p;
-  double* fr = a.fold + (size_t)c * (PSN_FOLD_HDR + 2 * K);
+  double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
   double* pd = (double*)prow;
   const int flags = a.flags;
   const double m = (double)p.T * (double)p.N;
@@ -421,6 +431,8 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       if (store) {
         fr[PSN_FOLD_HDR + i] = wf;
         fr[PSN_FOLD_HDR + K + i] = wq;
+        fr[PSN_FOLD_HDR + 2 * K + i] = tt[2 + i];      // sx
+        fr[PSN_FOLD_HDR + 3 * K + i] = tt[2 + K + i];  // sxh
       }
       pd[i] = wq;
     }
@@ -454,7 +466,8 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         double dw = aa * dwf[i];
-        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * tt[1 + K + i] + beta1 * tt[1 + 2 * K + i];
+        // BN term, network.py:298-315: sum_t x[t-off_i] dh1[t] = alpha1 sx + beta1 (sxh - mu* sx)
+        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * in.sx[i] + beta1 * (in.sxh[i] - mu * in.sx[i]);
         a.dW[(size_t)c * K + i] = dw;
       }
       a.dbeta[c] = db_f;
@@ -765,10 +778,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wr = a.shared ? 0 : cc;
     if constexpr (!BWD) {
 #pragma unroll
-      for (int i = 0; i < K; ++i) np1d[i] = cv ? __ldg(a.W + (size_t)wr * K + i) : 0.0;
+      for (int i = 0; i < K; ++i) {
+        np1d[i] = cv ? __ldg(a.W + (size_t)wr * K + i) : 0.0;
+        np1f[i] = (float)np1d[i];
+      }
       np1d[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments (pre-update running mean)
     } else {
-      const double* f = a.fold + (size_t)cc * (PSN_FOLD_HDR + 2 * K);
+      const double* f = a.fold + (size_t)cc * PSN_FOLD_STRIDE(K);
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         np1d[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;  // w_q
@@ -793,11 +809,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < NV; ++u) acc[u] = 0.0;
       if constexpr (!BWD) {
-        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
-        double w[K], xw[H + U], sh;
+        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps), plus
+        // the backward's BN-term sums sx[i] = sum x[t-off_i], sxh[i] = sum x[t-off_i] h1[t]
+        // (paired-free f32 on the otherwise idle FMA pipe, f64 across tiles)
+        double w[K], xw[H + U];
+        float wf[K], xf[H + U];
 #pragma unroll
-        for (int i = 0; i < K; ++i) w[i] = np1d[i];
-        sh = np1d[K];
+        for (int i = 0; i < K; ++i) {
+          w[i] = np1d[i];
+          wf[i] = np1f[i];
+        }
+        const double sh = np1d[K];
         if (g + 1 < p.G) prefetch_p1(g + 1);
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
@@ -807,28 +829,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)(nbi * kBoxN + n_in) < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+            for (int j = 0; j < H + U; ++j) {
+              xw[j] = 0.0;
+              xf[j] = 0.f;
+            }
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
+            for (int r = 0; r < H; ++r) {
+              xf[r] = ldsx<IO>(xs + (r) * RSB);
+              xw[r] = (double)xf[r];
+            }
             release_item();
           }
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
           double S1[U], S2[U];
+          float fsx[K], fsh[K];
 #pragma unroll
           for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
+#pragma unroll
+          for (int i = 0; i < K; ++i) fsx[i] = fsh[i] = 0.f;
           // full tiles (every row < T) run without per-row predicates
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
+              for (int u = 0; u < U; ++u) {
+                xf[H + u] = ldsx<IO>(xs + (r0 + u) * RSB);
+                xw[H + u] = (double)xf[H + u];
+              }
               double h[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
@@ -839,12 +873,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int u = 0; u < U; ++u) {
                 double hc = round_f32(h[u]) - sh;
-                if (!FULL) hc = (r0 + u < nvalid) ? hc : 0.0;
+                if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
                 S1[u] += hc;
                 S2[u] = fma(hc, hc, S2[u]);
               }
 #pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+              for (int u = 0; u < U; ++u) {
+                float h1 = wf[0] * xf[u + slot<K, D>(0)];
+#pragma unroll
+                for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
+                const bool ok = FULL || r0 + u < nvalid;
+                if (!ok) h1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  const float xi = xf[u + slot<K, D>(i)];
+                  if (FULL)
+                    fsx[i] += xi;
+                  else
+                    fsx[i] = ok ? fsx[i] + xi : fsx[i];
+                  fsh[i] = fmaf(xi, h1, fsh[i]);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < H; ++j) {
+                xw[j] = xw[j + U];
+                xf[j] = xf[j + U];
+              }
             }
           };
           if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
@@ -857,6 +911,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[0] += S1[u];
             acc[1] += S2[u];
           }
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            acc[2 + i] += (double)fsx[i];
+            acc[2 + K + i] += (double)fsh[i];
+          }
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
@@ -866,22 +925,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(nbi);
         }
       } else {
-        // ---- backward pass 1: db, dw_q (f64 end to end: h2 exact and f32-rounded like the
-        // reference's carrier, sigma' and dh2 in f64 -- f32 per-element errors (~1e-7) would
+        // ---- backward pass 1: db, dw_q -- f64 end to end (h2 exact and f32-rounded like the
+        // reference's carrier, sigma' and dh2 in f64): f32 per-element errors (~1e-7) would
         // grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5 bound on small dW
-        // entries); the BN-term sums sx, sxc reach dW through 1/m-scaled factors and use
-        // f32 within a tile.  Rows alternate between two f64 accumulator sets (ILP).
-        float w[K], xw[H + U];
+        // entries.  The BN-term sums come from the forward (fold row sx / sxh).  Rows
+        // alternate between two f64 accumulator sets (ILP).
         double wq[K], xd[H + U], acc2[1 + K];
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc2[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          wq[i] = np1d[i];
-          w[i] = np1f[i];
-        }
+        for (int i = 0; i < K; ++i) wq[i] = np1d[i];
         const double bf = np1d[K];
-        const float mu = np1f[K];
         if (g + 1 < p.G) prefetch_p1(g + 1);
         int tt = t_a % p.ttl;
         opaque(tt);
@@ -889,37 +943,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int t0 = tt * TB;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) {
-              xw[j] = 0.f;
-              xd[j] = 0.0;
-            }
+            for (int j = 0; j < H + U; ++j) xd[j] = 0.0;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) {
-              xw[r] = ldsx<IO>(xs + (r) * RSB);
-              xd[r] = (double)xw[r];
-            }
+            for (int r = 0; r < H; ++r) xd[r] = (double)ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const uint32_t ys = st + C_::XBYTES;
-          const int nvalid = min(TB, p.T - t0);
-          float fsx[K], fsc[K];
-#pragma unroll
-          for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
-          auto rows = [&](auto full_tag) {
-            constexpr bool FULL = decltype(full_tag)::value;
+          auto rows = [&]() {
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
               double yv[U], h2[U], dh[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
-                xd[H + u] = (double)xw[H + u];
+                xd[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
                 yv[u] = (double)ldsx<IO>(ys + ((r0 + u)) * RSB);  // rows >= T: TMA zero fill -> dh2 = 0
               }
 #pragma unroll
@@ -943,35 +985,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < K; ++i) A[1 + i] = fma(xd[u + slot<K, D>(i)], dh[u], A[1 + i]);
               }
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                float h1 = w[0] * xw[u + slot<K, D>(0)];
-#pragma unroll
-                for (int i = 1; i < K; ++i) h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
-                float hc = h1 - mu;
-                if (!FULL && !(r0 + u < nvalid)) hc = 0.f;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  const float xi = xw[u + slot<K, D>(i)];
-                  if (FULL)
-                    fsx[i] += xi;
-                  else
-                    fsx[i] = (r0 + u < nvalid) ? fsx[i] + xi : fsx[i];
-                  fsc[i] = fmaf(xi, hc, fsc[i]);
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < H; ++j) {
-                xw[j] = xw[j + U];
-                xd[j] = xd[j + U];
-              }
+              for (int j = 0; j < H; ++j) xd[j] = xd[j + U];
             }
           };
-          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            acc[1 + K + i] += (double)fsx[i];
-            acc[1 + 2 * K + i] += (double)fsc[i];
-          }
+          if (!(a.ablate & 1)) rows();
           release_item();
           if (++tt == p.ttl) tt = 0;
           opaque(tt);
