@@ -87,10 +87,11 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-// workspace: group counters | per-channel f64 sums (both zeroed per launch)
+// workspace: group counters (pass 1, pass 2) | per-channel f64 sums of pass 1 |
+// forward pass-2 sums -- all zeroed per launch
 static size_t zeroed_bytes(const Plan& p, bool bwd) {
-  const size_t nv = bwd ? 1 + (size_t)p.k : 2 + 2 * (size_t)p.k;
-  return a256(sizeof(unsigned) * p.G) + sizeof(double) * p.G * nv * kCols;
+  const Layout L = layout_of(p.k, p.d, 4, bwd);
+  return a256(2 * sizeof(unsigned) * p.G) + sizeof(double) * p.G * (L.NV + L.NV2) * kCols;
 }
 
 size_t workspace_bytes(const psn_desc_t* desc) {
@@ -126,13 +127,18 @@ int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const voi
 
 struct Ws {
   unsigned* cnt;
+  unsigned* cnt2;
   double* acc;
+  double* acc2;
 };
 
-static Ws carve(void* ws, const Plan& p) {
+static Ws carve(void* ws, const Plan& p, bool bwd) {
+  const Layout L = layout_of(p.k, p.d, 4, bwd);
   Ws w;
   w.cnt = (unsigned*)ws;
-  w.acc = (double*)((char*)ws + a256(sizeof(unsigned) * p.G));
+  w.cnt2 = w.cnt + p.G;
+  w.acc = (double*)((char*)ws + a256(2 * sizeof(unsigned) * p.G));
+  w.acc2 = w.acc + (size_t)p.G * L.NV * kCols;
   return w;
 }
 
@@ -145,7 +151,7 @@ static int dispatch(const psn_desc_t* desc, bool bwd, const Args& a, const void*
 
 int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* W, const double* gamma,
             const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st) {
-  Ws w = carve(ws, p);
+  Ws w = carve(ws, p, false);
   if (cudaMemsetAsync(ws, 0, zeroed_bytes(p, false), st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of stream counters failed");
   Args a;
@@ -160,6 +166,8 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
   a.fold = fold;
   a.cnt = w.cnt;
   a.acc = w.acc;
+  a.cnt2 = w.cnt2;
+  a.acc2 = w.acc2;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;
@@ -172,7 +180,7 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
 int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* dy, const double* W,
              const double* gamma, const double* fold, void* dx, double* dW, double* dgamma, double* dbeta,
              void* ws, cudaStream_t st) {
-  Ws w = carve(ws, p);
+  Ws w = carve(ws, p, true);
   if (cudaMemsetAsync(ws, 0, zeroed_bytes(p, true), st) != cudaSuccess)
     return fail(PSN_ERR_CUDA, "memset of stream counters failed");
   Args a;
@@ -187,6 +195,8 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
   a.dbeta = dbeta;
   a.cnt = w.cnt;
   a.acc = w.acc;
+  a.cnt2 = w.cnt2;
+  a.acc2 = w.acc2;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;

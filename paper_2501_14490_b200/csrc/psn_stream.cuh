@@ -101,6 +101,8 @@ struct Args {
   double* dbeta;
   double* acc;            // [G][NV][32] per-channel pass-1 sums (f64 atomic adds, zeroed per launch)
   unsigned* cnt;          // [G] pass-1 arrivals (every CTA arrives once per group)
+  double* acc2;           // [G][2k][32] forward pass-2 BN-term sums sx, sxh (f64 atomic adds, zeroed)
+  unsigned* cnt2;         // [G] forward pass-2 arrivals
   int flags;
   int shared;
   double eps, momentum;
@@ -279,23 +281,25 @@ __device__ __forceinline__ double rcp_f64(double v) {
 // planning (stage count) and the kernel both use it
 // -------------------------------------------------------------------------
 struct Layout {
-  int H, NV, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
+  int H, NV, NV2, TB, rowb, xbytes, dbytes, pstride, pbytes, stage, dep, tot, fixed;
 };
 __host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es == 4 ? PSN_TB_BWD : 2 * PSN_TB_BWD) : (es == 4 ? PSN_TB_FWD : 2 * PSN_TB_FWD); }
 __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
-  L.NV = bwd ? 1 + k : 2 + 2 * k;  // fwd: S1, S2, sx[k], sxh[k]; bwd: db, dw_q[k]
+  L.NV = bwd ? 1 + k : 2;   // pass-1 sums: fwd S1, S2; bwd db, dw_q[k]
+  L.NV2 = bwd ? 0 : 2 * k;  // forward pass-2 sums: sx[k], sxh[k]
   L.TB = tile_rows(es, bwd);
   L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
   L.xbytes = xrows * L.rowb;
   L.dbytes = bwd ? xrows * L.rowb : 0;
   // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
-  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
+  // per-lane pass-2 parameters: fwd f64 w_q[k], b_f + f32 W[k]; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
+  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : (8 * (k + 1) + 4 * k + 15) / 16 * 16;
   L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
   L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
-  L.dep = 8 * L.NV * kCols * 8;  // per-warp-pair partial sums handed to the publisher
+  L.dep = 8 * (L.NV > L.NV2 ? L.NV : L.NV2) * kCols * 8;  // per-warp-pair partial sums handed to the publisher
   L.tot = 8 * 2 * kCols * 8;                  // publisher ring: pre-update running stats of 8 groups
   L.fixed = L.dep + 4 * L.pbytes + L.tot + 512;
   return L;
@@ -431,10 +435,9 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       if (store) {
         fr[PSN_FOLD_HDR + i] = wf;
         fr[PSN_FOLD_HDR + K + i] = wq;
-        fr[PSN_FOLD_HDR + 2 * K + i] = tt[2 + i];      // sx
-        fr[PSN_FOLD_HDR + 3 * K + i] = tt[2 + K + i];  // sxh
       }
       pd[i] = wq;
+      ((float*)(prow + 8 * (K + 1)))[i] = (float)in.W[i];
     }
     pd[K] = bf;
   } else {
@@ -503,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C_ = Cfg<K, D, IO, BWD>;
   constexpr Layout LY = C_::L;
   constexpr int H = C_::H, NV = C_::NV, TB = C_::TB;
+  constexpr int kMaxNV = C_::L.NV > C_::L.NV2 ? C_::L.NV : C_::L.NV2;  // deposit slot stride
   const Plan& p = a.p;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -627,34 +631,54 @@ __global__ void __launch_bounds__(kThreads, 1)
       nrv = c < p.C ? __ldcg(a.rv + c) : 0.0;
     };
     if (!BWD && p.G > 0) prefetch_stats(0);
-    for (int it = 0; it < p.G; ++it) {
-      if (!BWD) {
-        prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
-        prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
-        if (it + 1 < p.G) prefetch_stats(it + 1);
-      }
-      const int v = worker_of(p, it, 0);
-      if (v < p.P) {
-        const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-        if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
-        __syncwarp();
-        if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
-        double t[NV];
+    auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
+      const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
+      if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
+      __syncwarp();
+      if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
 #pragma unroll
-        for (int val = 0; val < NV; ++val) {
-          double s = dep[(0 * NV + val) * kCols + lane];
+      for (int val = 0; val < kMaxNV; ++val) {
+        if (val < nv) {
+          double s = dep[(0 * kMaxNV + val) * kCols + lane];
 #pragma unroll
-          for (int w2 = 1; w2 < 8; ++w2) s += dep[(w2 * NV + val) * kCols + lane];
+          for (int w2 = 1; w2 < 8; ++w2) s += dep[(w2 * kMaxNV + val) * kCols + lane];
           t[val] = s;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(depe);
-#pragma unroll
-        for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
-        ++nd;
       }
       __syncwarp();
-      if (lane == 0) red_release(a.cnt + it, 1u);
+      if (lane == 0) mbar_arrive(depe);
+      ++nd;
+    };
+    for (int it = 0; it < iters; ++it) {
+      if (it < p.G) {
+        if (!BWD) {
+          prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
+          prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
+          if (it + 1 < p.G) prefetch_stats(it + 1);
+        }
+        if (worker_of(p, it, 0) < p.P) {
+          double t[kMaxNV];
+          take_deposit(NV, t);
+#pragma unroll
+          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
+        }
+        __syncwarp();
+        if (lane == 0) red_release(a.cnt + it, 1u);
+      }
+      if constexpr (!BWD) {  // forward pass-2 BN-term sums of group it - lag
+        const int g2 = it - p.lag;
+        if (g2 >= 0 && g2 < p.G) {
+          if (worker_of(p, g2, 1) < p.P) {
+            double t[kMaxNV];
+            take_deposit(LY.NV2, t);
+#pragma unroll
+            for (int val = 0; val < LY.NV2; ++val)
+              red_add_f64(a.acc2 + ((size_t)g2 * LY.NV2 + val) * kCols + lane, t[val]);
+          }
+          __syncwarp();
+          if (lane == 0) red_release(a.cnt2 + g2, 1u);
+        }
+      }
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
       printf("PSNTRACE %s publ cta %d total %llu dep %llu\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
@@ -702,6 +726,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(p2f + sl);
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
     }
+    if constexpr (!BWD) {  // the forward's BN-term sums, once every CTA streamed the group
+      for (int g = 0; g < p.G; ++g) {
+        if (designated_of(p, g) != (int)blockIdx.x) continue;
+        if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)p.nCTA, "pass-2 sums");
+        __syncwarp();
+        const int c = g * kCols + lane;
+        if (c < p.C) {
+          double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            fr[PSN_FOLD_HDR + 2 * K + i] = __ldcg(a.acc2 + ((size_t)g * LY.NV2 + i) * kCols + lane);
+            fr[PSN_FOLD_HDR + 3 * K + i] = __ldcg(a.acc2 + ((size_t)g * LY.NV2 + K + i) * kCols + lane);
+          }
+        }
+      }
+    }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
       printf("PSNTRACE %s fold cta %d total %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
              gtimer() - tf_start, tf_cnt, tf_fold);
@@ -746,19 +786,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   // per-warp pass-1 sums handed to the publisher: warps w and w + 8 share slot w
   // (the low warp stores, the high warp adds in fixed order and arrives)
-  auto deposit = [&](const double* acc) {
+  auto deposit = [&](const double* acc, int nv) {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     if (nd >= 1) mbar_wait<64>(depe, (unsigned)((nd - 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
     const int sw = warp & 7;
     if (warp < 8) {
 #pragma unroll
-      for (int val = 0; val < NV; ++val) dep[(sw * NV + val) * kCols + lane] = acc[val];
+      for (int val = 0; val < kMaxNV; ++val)
+        if (val < nv) dep[(sw * kMaxNV + val) * kCols + lane] = acc[val];
     }
     asm volatile("bar.sync %0, 64;" ::"r"(2 + sw) : "memory");  // pair barrier (warps sw, sw + 8)
     if (warp >= 8) {
 #pragma unroll
-      for (int val = 0; val < NV; ++val) dep[(sw * NV + val) * kCols + lane] += acc[val];
+      for (int val = 0; val < kMaxNV; ++val)
+        if (val < nv) dep[(sw * kMaxNV + val) * kCols + lane] += acc[val];
       __syncwarp();
       if (lane == 0) mbar_arrive(depf);
     }
@@ -809,16 +851,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < NV; ++u) acc[u] = 0.0;
       if constexpr (!BWD) {
-        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps), plus
-        // the backward's BN-term sums sx[i] = sum x[t-off_i], sxh[i] = sum x[t-off_i] h1[t]
-        // (paired-free f32 on the otherwise idle FMA pipe, f64 across tiles)
+        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
         double w[K], xw[H + U];
-        float wf[K], xf[H + U];
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          w[i] = np1d[i];
-          wf[i] = np1f[i];
-        }
+        for (int i = 0; i < K; ++i) w[i] = np1d[i];
         const double sh = np1d[K];
         if (g + 1 < p.G) prefetch_p1(g + 1);
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
@@ -829,40 +865,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)(nbi * kBoxN + n_in) < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) {
-              xw[j] = 0.0;
-              xf[j] = 0.f;
-            }
+            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) {
-              xf[r] = ldsx<IO>(xs + (r) * RSB);
-              xw[r] = (double)xf[r];
-            }
+            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
-          double S1[U], S2[U];
-          float fsx[K], fsh[K];
-#pragma unroll
-          for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
-#pragma unroll
-          for (int i = 0; i < K; ++i) fsx[i] = fsh[i] = 0.f;
+          double S1[2], S2[2];  // two alternating sets (ILP without a U-fold register cost)
+          S1[0] = S1[1] = S2[0] = S2[1] = 0.0;
           // full tiles (every row < T) run without per-row predicates
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                xf[H + u] = ldsx<IO>(xs + (r0 + u) * RSB);
-                xw[H + u] = (double)xf[H + u];
-              }
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + (r0 + u) * RSB);
               double h[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
@@ -874,47 +897,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 double hc = round_f32(h[u]) - sh;
                 if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
-                S1[u] += hc;
-                S2[u] = fma(hc, hc, S2[u]);
+                S1[u & 1] += hc;
+                S2[u & 1] = fma(hc, hc, S2[u & 1]);
               }
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                float h1 = wf[0] * xf[u + slot<K, D>(0)];
-#pragma unroll
-                for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
-                const bool ok = FULL || r0 + u < nvalid;
-                if (!ok) h1 = 0.f;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  const float xi = xf[u + slot<K, D>(i)];
-                  if (FULL)
-                    fsx[i] += xi;
-                  else
-                    fsx[i] = ok ? fsx[i] + xi : fsx[i];
-                  fsh[i] = fmaf(xi, h1, fsh[i]);
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < H; ++j) {
-                xw[j] = xw[j + U];
-                xf[j] = xf[j + U];
-              }
+              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
           };
           if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
-          if (!lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
-#pragma unroll
-            for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            acc[0] += S1[u];
-            acc[1] += S2[u];
-          }
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            acc[2 + i] += (double)fsx[i];
-            acc[2 + K + i] += (double)fsh[i];
+          if (lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
+            acc[0] += S1[0] + S1[1];
+            acc[1] += S2[0] + S2[1];
           }
           release_item();
           if (++tt == p.ttl) {
@@ -996,7 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
       }
-      if (v < p.P) deposit(acc);  // CTA reduction + publication happen on the publisher warp
+      if (v < p.P) deposit(acc, NV);  // CTA reduction + publication happen on the publisher warp
     }
     // ------------------------------------------------------------- pass 2
     if (it >= p.lag && it - p.lag < p.G) {
@@ -1009,13 +1002,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (v >= p.P) t_a = t_b = 0;
       IO* out = (IO*)a.out;
       if constexpr (!BWD) {
-        // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
-        double wq[K], xw[H + U];
+        // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]; power-of-two
+        // products are exact, so the f64 DFMA chain equals the reference's mul-then-add sum.
+        // The same pass forms the backward's BN-term sums sx[i] = sum x[t-off_i] and
+        // sxh[i] = sum x[t-off_i] h1[t] (f32 per tile on the FMA pipe, f64 across tiles)
+        double wq[K], xw[H + U], sacc[2 * K];
+        float wf[K], xf[H + U];
         const double* pd = (const double*)pr;
+        const float* pf = (const float*)(pr + 8 * (K + 1));
 #pragma unroll
-        for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
+        for (int i = 0; i < K; ++i) {
+          wq[i] = ldsd(pd + i);
+          wf[i] = ldsf(pf + i);
+        }
         const double bf = ldsd(pd + K);
         done_params(g);
+#pragma unroll
+        for (int i = 0; i < 2 * K; ++i) sacc[i] = 0.0;
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -1025,26 +1028,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)n < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+            for (int j = 0; j < H + U; ++j) {
+              xw[j] = 0.0;
+              xf[j] = 0.f;
+            }
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
+            for (int r = 0; r < H; ++r) {
+              xf[r] = ldsx<IO>(xs + (r) * RSB);
+              xw[r] = (double)xf[r];
+            }
             release_item();
           }
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
           uint32_t ooff = ((uint32_t)t0 * mN + (uint32_t)(lv ? n : 0)) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
+          float fsx[K], fsh[K];
+#pragma unroll
+          for (int i = 0; i < K; ++i) fsx[i] = fsh[i] = 0.f;
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
-              double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
+              for (int u = 0; u < U; ++u) {
+                xf[H + u] = ldsx<IO>(xs + (r0 + u) * RSB);
+                xw[H + u] = (double)xf[H + u];
+              }
+              double h[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
@@ -1055,14 +1070,36 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
                 const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-                if (lv && (FULL || r0 + u < nvalid)) st_out(out + ooff, sp, pol_out);
+                const bool ok = FULL || r0 + u < nvalid;
+                if (lv && ok) st_out(out + ooff, sp, pol_out);
                 ooff += rs32;
+                float h1 = wf[0] * xf[u + slot<K, D>(0)];
+#pragma unroll
+                for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
+                if (!ok) h1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  const float xi = xf[u + slot<K, D>(i)];
+                  if (FULL)
+                    fsx[i] += xi;
+                  else
+                    fsx[i] = ok ? fsx[i] + xi : fsx[i];
+                  fsh[i] = fmaf(xi, h1, fsh[i]);
+                }
               }
 #pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+              for (int j = 0; j < H; ++j) {
+                xw[j] = xw[j + U];
+                xf[j] = xf[j + U];
+              }
             }
           };
           if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+#pragma unroll
+          for (int i = 0; i < K; ++i) {  // padding streams read TMA zero fill: zero contributions
+            sacc[i] += (double)fsx[i];
+            sacc[K + i] += (double)fsh[i];
+          }
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
@@ -1071,6 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
+        if (v < p.P) deposit(sacc, 2 * K);
       } else {
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
