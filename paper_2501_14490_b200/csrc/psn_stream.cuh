@@ -53,6 +53,7 @@ constexpr int kCols = 32;                        // columns per tile (lanes)
 constexpr int kBoxN = kConsumerWarps;            // batch rows per tile: consumer warp w owns row w
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
 constexpr int kRowBlock = 4;                     // time rows a consumer thread advances at once (ILP)
+constexpr int kRowBlockF2 = 2;                   // ... in the forward's second pass
 
 #ifndef PSN_TB_FWD
 #define PSN_TB_FWD 32  // f32 time rows per forward tile (bf16: twice)
@@ -107,7 +108,7 @@ struct Args {
   int shared;
   double eps, momentum;
   Surrogate sur;    // f32 surrogate (dx pass)
-  int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA
+  int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA, 16 no pass-2 deposit
   int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
   double sc, sscale; // f64 surrogate: arctan c = pi*alpha/2, scale = alpha/2; rational c = alpha, scale = 1
   int skind;
@@ -650,7 +651,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++nd;
     };
     for (int it = 0; it < iters; ++it) {
-      if (it < p.G) {
+      const bool p1 = it < p.G;
+      const int g2 = it - p.lag;
+      const bool p2 = !BWD && g2 >= 0 && g2 < p.G;  // forward pass-2 BN-term sums of group it - lag
+      if (p1) {
         if (!BWD) {
           prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
           prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
@@ -662,22 +666,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
         }
-        __syncwarp();
-        if (lane == 0) red_release(a.cnt + it, 1u);
       }
-      if constexpr (!BWD) {  // forward pass-2 BN-term sums of group it - lag
-        const int g2 = it - p.lag;
-        if (g2 >= 0 && g2 < p.G) {
-          if (worker_of(p, g2, 1) < p.P) {
-            double t[kMaxNV];
-            take_deposit(LY.NV2, t);
+      if constexpr (!BWD) {
+        if (p2 && worker_of(p, g2, 1) < p.P && !(a.ablate & 16)) {
+          double t[kMaxNV];
+          take_deposit(LY.NV2, t);
 #pragma unroll
-            for (int val = 0; val < LY.NV2; ++val)
-              red_add_f64(a.acc2 + ((size_t)g2 * LY.NV2 + val) * kCols + lane, t[val]);
-          }
-          __syncwarp();
-          if (lane == 0) red_release(a.cnt2 + g2, 1u);
+          for (int val = 0; val < LY.NV2; ++val)
+            red_add_f64(a.acc2 + ((size_t)g2 * LY.NV2 + val) * kCols + lane, t[val]);
         }
+      }
+      // one release fence for this iteration's atomics, then relaxed arrivals
+      __syncwarp();
+      if (lane == 0 && (p1 || p2)) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (p1) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + it) : "memory");
+        if (p2) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt2 + g2) : "memory");
       }
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
@@ -877,8 +881,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
-          double S1[2], S2[2];  // two alternating sets (ILP without a U-fold register cost)
-          S1[0] = S1[1] = S2[0] = S2[1] = 0.0;
+          double S1[U], S2[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) S1[u] = S2[u] = 0.0;
           // full tiles (every row < T) run without per-row predicates
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
@@ -897,8 +902,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 double hc = round_f32(h[u]) - sh;
                 if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
-                S1[u & 1] += hc;
-                S2[u & 1] = fma(hc, hc, S2[u & 1]);
+                S1[u] += hc;
+                S2[u] = fma(hc, hc, S2[u]);
               }
 #pragma unroll
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
@@ -906,8 +911,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           };
           if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           if (lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
-            acc[0] += S1[0] + S1[1];
-            acc[1] += S2[0] + S2[1];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              acc[0] += S1[u];
+              acc[1] += S2[u];
+            }
           }
           release_item();
           if (++tt == p.ttl) {
@@ -1004,8 +1012,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!BWD) {
         // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]; power-of-two
         // products are exact, so the f64 DFMA chain equals the reference's mul-then-add sum.
-        // The same pass forms the backward's BN-term sums sx[i] = sum x[t-off_i] and
-        // sxh[i] = sum x[t-off_i] h1[t] (f32 per tile on the FMA pipe, f64 across tiles)
+        // The same pass forms the backward's BN-term sums sx[i] = sum_t x[t-off_i] and
+        // sxh[i] = sum_t x[t-off_i] h1[t] = sum_j W_j sum_t x[t-off_i] x[t-off_j].  Over a run of
+        // full tiles they come from one running sum X = sum x[t] and k lag products
+        // P[m] = sum x[t] x[t-m d] (f32 per tile, f64 across), plus head / tail corrections
+        // at the run's ends from the register window; partial (last) tiles sum directly.
+        constexpr int U = kRowBlockF2;  // short DFMA chain: fewer rows per block, fewer live registers
         double wq[K], xw[H + U], sacc[2 * K];
         float wf[K], xf[H + U];
         const double* pd = (const double*)pr;
@@ -1019,6 +1031,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         done_params(g);
 #pragma unroll
         for (int i = 0; i < 2 * K; ++i) sacc[i] = 0.0;
+        // boundary terms of a full-tile run: sign +1 at its start, -1 after its end; the
+        // window holds the H rows before that boundary (xf[H - q] = x[edge - q])
+        auto edge = [&](float sgn) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const int oi = (K - 1 - i) * D;
+            float ex = 0.f;
+#pragma unroll
+            for (int q = 1; q <= oi; ++q) ex += xf[H - q];
+            float eh = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              const int o = (K - 1 - (i > j ? i : j)) * D, dl = (i > j ? i - j : j - i) * D;
+              float e = 0.f;
+#pragma unroll
+              for (int q = 1; q <= o; ++q) e = fmaf(xf[H - q], xf[H - q - dl], e);
+              eh = fmaf(wf[j], e, eh);
+            }
+            sacc[i] += (double)(sgn * ex);
+            sacc[K + i] += (double)(sgn * eh);
+          }
+        };
+        bool open_run = false;
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -1046,10 +1081,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
+          const bool full_tile = nvalid == TB;
+          if (full_tile && !open_run) {
+            edge(1.f);
+            open_run = true;
+          }
           uint32_t ooff = ((uint32_t)t0 * mN + (uint32_t)(lv ? n : 0)) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
-          float fsx[K], fsh[K];
+          float fX = 0.f, fP[K], fsx[K], fsh[K];
 #pragma unroll
-          for (int i = 0; i < K; ++i) fsx[i] = fsh[i] = 0.f;
+          for (int i = 0; i < K; ++i) fP[i] = fsx[i] = fsh[i] = 0.f;
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
@@ -1073,18 +1113,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool ok = FULL || r0 + u < nvalid;
                 if (lv && ok) st_out(out + ooff, sp, pol_out);
                 ooff += rs32;
-                float h1 = wf[0] * xf[u + slot<K, D>(0)];
+                const float xc = xf[u + H];
+                if (FULL) {  // running sum and lag products
+                  fX += xc;
 #pragma unroll
-                for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
-                if (!ok) h1 = 0.f;
+                  for (int m = 0; m < K; ++m) fP[m] = fmaf(xc, xf[u + H - m * D], fP[m]);
+                } else {     // direct sums over the valid rows
+                  float h1 = wf[0] * xf[u + slot<K, D>(0)];
 #pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  const float xi = xf[u + slot<K, D>(i)];
-                  if (FULL)
-                    fsx[i] += xi;
-                  else
+                  for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
+                  if (!ok) h1 = 0.f;
+#pragma unroll
+                  for (int i = 0; i < K; ++i) {
+                    const float xi = xf[u + slot<K, D>(i)];
                     fsx[i] = ok ? fsx[i] + xi : fsx[i];
-                  fsh[i] = fmaf(xi, h1, fsh[i]);
+                    fsh[i] = fmaf(xi, h1, fsh[i]);
+                  }
                 }
               }
 #pragma unroll
@@ -1094,13 +1138,32 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
-          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if (a.ablate & 1) {
+          } else if (full_tile) {
+            rows(std::true_type{});
 #pragma unroll
-          for (int i = 0; i < K; ++i) {  // padding streams read TMA zero fill: zero contributions
-            sacc[i] += (double)fsx[i];
-            sacc[K + i] += (double)fsh[i];
+            for (int i = 0; i < K; ++i) {
+              float sh_i = 0.f;
+#pragma unroll
+              for (int j = 0; j < K; ++j) sh_i = fmaf(wf[j], fP[i > j ? i - j : j - i], sh_i);
+              sacc[i] += (double)fX;
+              sacc[K + i] += (double)sh_i;
+            }
+          } else {
+            rows(std::false_type{});
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              sacc[i] += (double)fsx[i];
+              sacc[K + i] += (double)fsh[i];
+            }
           }
           release_item();
+          // a run of full tiles ends before a new stream, a partial tile or the range end
+          const bool next_new = tile + 1 == t_b || tt + 1 == p.ttl || ((tt + 2) * TB > p.T);
+          if (open_run && next_new) {
+            edge(-1.f);
+            open_run = false;
+          }
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
@@ -1108,7 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
-        if (v < p.P) deposit(sacc, 2 * K);
+        if (v < p.P && !(a.ablate & 16)) deposit(sacc, 2 * K);
       } else {
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
