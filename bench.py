@@ -188,7 +188,7 @@ def main():
     ws = L.workspace(desc, dev)
     out = torch.empty_like(x)
     dx = torch.empty_like(x)
-    fold = torch.empty((C, L.PSN_FOLD_HDR + 4 * k), dtype=torch.float64, device=dev)
+    fold = torch.empty((C, L.PSN_FOLD_HDR + 2 * k), dtype=torch.float64, device=dev)
     grads = torch.empty(C * k + 2 * C, dtype=torch.float64, device=dev)  # one flat DDP bucket
     dW, dgam, dbet = grads[:C * k], grads[C * k:C * k + C], grads[C * k + C:]
     stream = torch.cuda.current_stream(dev)

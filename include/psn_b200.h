@@ -85,12 +85,9 @@ typedef struct {
 
 /* Per-channel forward state ("fold") the backward consumes; float64,
  * psn_fold_doubles(desc) values = C * PSN_FOLD_STRIDE(k), row c:
- *   [mu*, s, a, b_f, mu_batch, var_batch, w_f[0..k), w_q[0..k), sx[0..k), sxh[0..k)]
- * sx[i] = sum_t x[t-off_i], sxh[i] = sum_t x[t-off_i] h1[t] over all (t, n, q): the
- * BN-term sums of the backward's weight gradient, formed in the forward's first
- * pass (the reference keeps h1 in SpikingLayer._cache for the same purpose).     */
+ *   [mu*, s, a, b_f, mu_batch, var_batch, w_f[0..k), w_q[0..k)]                */
 #define PSN_FOLD_HDR 6
-#define PSN_FOLD_STRIDE(k) (PSN_FOLD_HDR + 4 * (k))
+#define PSN_FOLD_STRIDE(k) (PSN_FOLD_HDR + 2 * (k))
 
 PSN_API const char *psn_last_error(void);          /* thread-local message of last failure */
 PSN_API int psn_abi_version(void);

@@ -102,8 +102,8 @@ struct Args {
   double* dbeta;
   double* acc;            // [G][NV][32] per-channel pass-1 sums (f64 atomic adds, zeroed per launch)
   unsigned* cnt;          // [G] pass-1 arrivals (every CTA arrives once per group)
-  double* acc2;           // [G][2k][32] forward pass-2 BN-term sums sx, sxh (f64 atomic adds, zeroed)
-  unsigned* cnt2;         // [G] forward pass-2 arrivals
+  double* acc2;           // [G][2k][32] backward pass-2 BN-term sums sx, sxc (f64 atomic adds, zeroed)
+  unsigned* cnt2;         // [G] backward pass-2 arrivals
   int flags;
   int shared;
   double eps, momentum;
@@ -289,15 +289,15 @@ __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
   L.NV = bwd ? 1 + k : 2;   // pass-1 sums: fwd S1, S2; bwd db, dw_q[k]
-  L.NV2 = bwd ? 0 : 2 * k;  // forward pass-2 sums: sx[k], sxh[k]
+  L.NV2 = bwd ? 2 * k : 0;  // backward pass-2 BN-term sums: sx[k], sxc[k]
   L.TB = tile_rows(es, bwd);
   L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
   L.xbytes = xrows * L.rowb;
   L.dbytes = bwd ? xrows * L.rowb : 0;
   // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
-  // per-lane pass-2 parameters: fwd f64 w_q[k], b_f + f32 W[k]; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
-  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : (8 * (k + 1) + 4 * k + 15) / 16 * 16;
+  // per-lane pass-2 parameters: fwd f64 w_q[k], b_f; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
+  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
   L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
   L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
   L.dep = 8 * (L.NV > L.NV2 ? L.NV : L.NV2) * kCols * 8;  // per-warp-pair partial sums handed to the publisher
@@ -353,7 +353,6 @@ template <int K, bool BWD>
 struct FoldIn {
   double W[K], gamma, beta;
   double mu, s, aa, bf, wf[BWD ? K : 1], wq[BWD ? K : 1];  // the forward's fold row (backward only)
-  double sx[BWD ? K : 1], sxh[BWD ? K : 1];                 // BN-term sums cached by the forward
 };
 template <int K, bool BWD>
 __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD>& in) {
@@ -373,8 +372,6 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
     for (int i = 0; i < K; ++i) {
       in.wf[i] = __ldg(fr + PSN_FOLD_HDR + i);
       in.wq[i] = __ldg(fr + PSN_FOLD_HDR + K + i);
-      in.sx[i] = __ldg(fr + PSN_FOLD_HDR + 2 * K + i);
-      in.sxh[i] = __ldg(fr + PSN_FOLD_HDR + 3 * K + i);
     }
   }
 }
@@ -388,7 +385,8 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
 // -------------------------------------------------------------------------
 template <int K, bool BWD>
 __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<K, BWD>& in, const double* tt,
-                                             double rm_prev, double rv_prev, bool store, unsigned char* prow) {
+                                             double rm_prev, double rv_prev, bool store, unsigned char* prow,
+                                             const double* sxs = nullptr) {
   const Plan& p = a.p;
   double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
   double* pd = (double*)prow;
@@ -438,7 +436,6 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
         fr[PSN_FOLD_HDR + K + i] = wq;
       }
       pd[i] = wq;
-      ((float*)(prow + 8 * (K + 1)))[i] = (float)in.W[i];
     }
     pd[K] = bf;
   } else {
@@ -466,14 +463,16 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       alpha1 = dmu / m;
       beta1 = (2.0 / m) * dvar;
     }
-    if (store) {
+    if (sxs != nullptr) {  // kernel tail: dW with the BN term from the pass-2 sums sx, sxc
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         double dw = aa * dwf[i];
-        // BN term, network.py:298-315: sum_t x[t-off_i] dh1[t] = alpha1 sx + beta1 (sxh - mu* sx)
-        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * in.sx[i] + beta1 * (in.sxh[i] - mu * in.sx[i]);
+        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * sxs[i] + beta1 * sxs[K + i];  // network.py:298-315
         a.dW[(size_t)c * K + i] = dw;
       }
+      return;
+    }
+    if (store) {
       a.dbeta[c] = db_f;
       a.dgamma[c] = da / s;
     }
@@ -653,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; it < iters; ++it) {
       const bool p1 = it < p.G;
       const int g2 = it - p.lag;
-      const bool p2 = !BWD && g2 >= 0 && g2 < p.G;  // forward pass-2 BN-term sums of group it - lag
+      const bool p2 = BWD && g2 >= 0 && g2 < p.G;  // backward pass-2 BN-term sums of group it - lag
       if (p1) {
         if (!BWD) {
           prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
@@ -667,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
         }
       }
-      if constexpr (!BWD) {
+      if constexpr (BWD) {
         if (p2 && worker_of(p, g2, 1) < p.P && !(a.ablate & 16)) {
           double t[kMaxNV];
           take_deposit(LY.NV2, t);
@@ -730,19 +729,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(p2f + sl);
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
     }
-    if constexpr (!BWD) {  // the forward's BN-term sums, once every CTA streamed the group
+    if constexpr (BWD) {  // dW once every CTA streamed the group's pass 2 (BN-term sums sx, sxc)
       for (int g = 0; g < p.G; ++g) {
         if (designated_of(p, g) != (int)blockIdx.x) continue;
+        const int c = g * kCols + lane;
+        FoldIn<K, BWD> in;
+        if (c < p.C) load_fold_in<K, BWD>(a, c, in);
         if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)p.nCTA, "pass-2 sums");
         __syncwarp();
-        const int c = g * kCols + lane;
         if (c < p.C) {
-          double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
+          double tt[NV], sxs[2 * K];
 #pragma unroll
-          for (int i = 0; i < K; ++i) {
-            fr[PSN_FOLD_HDR + 2 * K + i] = __ldcg(a.acc2 + ((size_t)g * LY.NV2 + i) * kCols + lane);
-            fr[PSN_FOLD_HDR + 3 * K + i] = __ldcg(a.acc2 + ((size_t)g * LY.NV2 + K + i) * kCols + lane);
-          }
+          for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
+#pragma unroll
+          for (int i = 0; i < 2 * K; ++i) sxs[i] = __ldcg(a.acc2 + ((size_t)g * 2 * K + i) * kCols + lane);
+          fold_channel<K, BWD>(a, c, in, tt, 0.0, 0.0, true, nullptr, sxs);
         }
       }
     }
@@ -1010,50 +1011,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (v >= p.P) t_a = t_b = 0;
       IO* out = (IO*)a.out;
       if constexpr (!BWD) {
-        // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]; power-of-two
-        // products are exact, so the f64 DFMA chain equals the reference's mul-then-add sum.
-        // The same pass forms the backward's BN-term sums sx[i] = sum_t x[t-off_i] and
-        // sxh[i] = sum_t x[t-off_i] h1[t] = sum_j W_j sum_t x[t-off_i] x[t-off_j].  Over a run of
-        // full tiles they come from one running sum X = sum x[t] and k lag products
-        // P[m] = sum x[t] x[t-m d] (f32 per tile, f64 across), plus head / tail corrections
-        // at the run's ends from the register window; partial (last) tiles sum directly.
-        constexpr int U = kRowBlockF2;  // short DFMA chain: fewer rows per block, fewer live registers
-        double wq[K], xw[H + U], sacc[2 * K];
-        float wf[K], xf[H + U];
+        // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
+        double wq[K], xw[H + U];
         const double* pd = (const double*)pr;
-        const float* pf = (const float*)(pr + 8 * (K + 1));
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          wq[i] = ldsd(pd + i);
-          wf[i] = ldsf(pf + i);
-        }
+        for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
         const double bf = ldsd(pd + K);
         done_params(g);
-#pragma unroll
-        for (int i = 0; i < 2 * K; ++i) sacc[i] = 0.0;
-        // boundary terms of a full-tile run: sign +1 at its start, -1 after its end; the
-        // window holds the H rows before that boundary (xf[H - q] = x[edge - q])
-        auto edge = [&](float sgn) {
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            const int oi = (K - 1 - i) * D;
-            float ex = 0.f;
-#pragma unroll
-            for (int q = 1; q <= oi; ++q) ex += xf[H - q];
-            float eh = 0.f;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              const int o = (K - 1 - (i > j ? i : j)) * D, dl = (i > j ? i - j : j - i) * D;
-              float e = 0.f;
-#pragma unroll
-              for (int q = 1; q <= o; ++q) e = fmaf(xf[H - q], xf[H - q - dl], e);
-              eh = fmaf(wf[j], e, eh);
-            }
-            sacc[i] += (double)(sgn * ex);
-            sacc[K + i] += (double)(sgn * eh);
-          }
-        };
-        bool open_run = false;
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -1063,43 +1027,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)n < mN && col < p.J;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) {
-              xw[j] = 0.0;
-              xf[j] = 0.f;
-            }
+            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) {
-              xf[r] = ldsx<IO>(xs + (r) * RSB);
-              xw[r] = (double)xf[r];
-            }
+            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
           const uint32_t st = wait_item();
           const uint32_t xs = st;
           const int nvalid = min(TB, p.T - t0);
-          const bool full_tile = nvalid == TB;
-          if (full_tile && !open_run) {
-            edge(1.f);
-            open_run = true;
-          }
           uint32_t ooff = ((uint32_t)t0 * mN + (uint32_t)(lv ? n : 0)) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
-          float fX = 0.f, fP[K], fsx[K], fsh[K];
-#pragma unroll
-          for (int i = 0; i < K; ++i) fP[i] = fsx[i] = fsh[i] = 0.f;
           auto rows = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                xf[H + u] = ldsx<IO>(xs + (r0 + u) * RSB);
-                xw[H + u] = (double)xf[H + u];
-              }
-              double h[U];
+              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
+              double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
@@ -1110,60 +1057,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < U; ++u) {
                 // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
                 const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-                const bool ok = FULL || r0 + u < nvalid;
-                if (lv && ok) st_out(out + ooff, sp, pol_out);
+                if (lv && (FULL || r0 + u < nvalid)) st_out(out + ooff, sp, pol_out);
                 ooff += rs32;
-                const float xc = xf[u + H];
-                if (FULL) {  // running sum and lag products
-                  fX += xc;
-#pragma unroll
-                  for (int m = 0; m < K; ++m) fP[m] = fmaf(xc, xf[u + H - m * D], fP[m]);
-                } else {     // direct sums over the valid rows
-                  float h1 = wf[0] * xf[u + slot<K, D>(0)];
-#pragma unroll
-                  for (int i = 1; i < K; ++i) h1 = fmaf(wf[i], xf[u + slot<K, D>(i)], h1);
-                  if (!ok) h1 = 0.f;
-#pragma unroll
-                  for (int i = 0; i < K; ++i) {
-                    const float xi = xf[u + slot<K, D>(i)];
-                    fsx[i] = ok ? fsx[i] + xi : fsx[i];
-                    fsh[i] = fmaf(xi, h1, fsh[i]);
-                  }
-                }
               }
 #pragma unroll
-              for (int j = 0; j < H; ++j) {
-                xw[j] = xw[j + U];
-                xf[j] = xf[j + U];
-              }
+              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
           };
-          if (a.ablate & 1) {
-          } else if (full_tile) {
-            rows(std::true_type{});
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-              float sh_i = 0.f;
-#pragma unroll
-              for (int j = 0; j < K; ++j) sh_i = fmaf(wf[j], fP[i > j ? i - j : j - i], sh_i);
-              sacc[i] += (double)fX;
-              sacc[K + i] += (double)sh_i;
-            }
-          } else {
-            rows(std::false_type{});
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-              sacc[i] += (double)fsx[i];
-              sacc[K + i] += (double)fsh[i];
-            }
-          }
+          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           release_item();
-          // a run of full tiles ends before a new stream, a partial tile or the range end
-          const bool next_new = tile + 1 == t_b || tt + 1 == p.ttl || ((tt + 2) * TB > p.T);
-          if (open_run && next_new) {
-            edge(-1.f);
-            open_run = false;
-          }
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
@@ -1171,7 +1073,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
-        if (v < p.P && !(a.ablate & 16)) deposit(sacc, 2 * K);
       } else {
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
@@ -1194,7 +1095,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto emit = [&](int od, float val) {
           if (lv && od >= run_t0 && od < p.T) st_out(out + (obase + (uint32_t)od * rs32), val, pol_out);
         };
-        auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1) {
+        // BN-term sums of this range (network.py:298-315): sx[i] = sum_t x[t-off_i],
+        // sxc[i] = sum_t x[t-off_i] (h1[t] - mu*); f32 per tile, f64 across tiles
+        double sacc[kMaxNV];
+#pragma unroll
+        for (int i = 0; i < kMaxNV; ++i) sacc[i] = 0.0;
+        float fsx[K], fsc[K];
+        auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1, bool sum) {
           float h1 = w[0] * xw[u + slot<K, D>(0)], h2 = wq[0] * xw[u + slot<K, D>(0)];
 #pragma unroll
           for (int i = 1; i < K; ++i) {
@@ -1202,14 +1109,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             h2 = fmaf(wq[i], xw[u + slot<K, D>(i)], h2);
           }
           h2 += bf;
+          const float hc = h1 - mu;
           dh2 = ok ? yv * surrogate_grad(a.sur, h2) : 0.f;
-          dh1 = ok ? fmaf(b1, h1 - mu, a1) : 0.f;
+          dh1 = ok ? fmaf(b1, hc, a1) : 0.f;
+          if (sum && ok) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              fsx[i] += xw[u + slot<K, D>(i)];
+              fsc[i] = fmaf(xw[u + slot<K, D>(i)], hc, fsc[i]);
+            }
+          }
         };
         // single-row step (TAIL rows): scatter, emit the row H behind, shift by one
         auto step1 = [&](float xv, float yv, bool ok, int tcur) {
           xw[H] = xv;
           float dh2, dh1;
-          dh_row(0, yv, ok, dh2, dh1);
+          dh_row(0, yv, ok, dh2, dh1, false);  // TAIL rows belong to the next range's sums
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             pacc[slot<K, D>(i)] = fmaf(wq[i], dh2, pacc[slot<K, D>(i)]);
@@ -1265,7 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u) xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                  dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u]);
+                  dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u], true);
 #pragma unroll
                 for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -1288,7 +1203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
               }
             };
+#pragma unroll
+            for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
             if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              sacc[i] += (double)fsx[i];
+              sacc[K + i] += (double)fsc[i];
+            }
           }
           release_item();
           if constexpr (H > 0) {
@@ -1312,6 +1234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
+        if (v < p.P && !(a.ablate & 16)) deposit(sacc, 2 * K);
       }
     }
   }

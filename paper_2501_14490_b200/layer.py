@@ -53,7 +53,7 @@ class _PSNFunction(torch.autograd.Function):
         desc = L.make_desc(x.shape, *desc_args)
         lib = L.lib()
         out = torch.empty_like(x)
-        fold = torch.empty((x.shape[2], L.PSN_FOLD_HDR + 4 * desc.k), dtype=torch.float64, device=x.device)
+        fold = torch.empty((x.shape[2], L.PSN_FOLD_HDR + 2 * desc.k), dtype=torch.float64, device=x.device)
         ws = L.workspace(desc, x.device)
         L.check(lib.psn_forward_train(ctypes.byref(desc), L.ptr(x), L.ptr(W), L.ptr(gamma), L.ptr(beta),
                                       L.ptr(running_mean), L.ptr(running_var), L.ptr(out), L.ptr(fold),
