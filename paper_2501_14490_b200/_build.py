@@ -49,20 +49,27 @@ def _stamp() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every CUDA source for sm_100a and link libpsn_b200.so."""
-    os.makedirs(OUT_DIR, exist_ok=True)
-    stamp_path = os.path.join(OUT_DIR, "build.stamp")
-    stamp = _stamp()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp_path):
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Compile every CUDA source for sm_100a and link libpsn_b200.so.
+
+    ``trace=True`` builds the per-CTA wait/compute tracing variant
+    (-DPSN_TRACE_BUILD=1) into ``_lib_trace/``; load it with PSN_B200_LIB.
+    """
+    out_dir = OUT_DIR + ("_trace" if trace else "")
+    lib_path = os.path.join(out_dir, "libpsn_b200.so")
+    extra = ["-DPSN_TRACE_BUILD=1"] if trace else []
+    os.makedirs(out_dir, exist_ok=True)
+    stamp_path = os.path.join(out_dir, "build.stamp")
+    stamp = _stamp() + (" trace" if trace else "")
+    if not force and os.path.exists(lib_path) and os.path.exists(stamp_path):
         if open(stamp_path).read().strip() == stamp:
-            return LIB
+            return lib_path
     nvcc = _nvcc()
     objs = []
 
     def compile_one(src):
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        obj = os.path.join(out_dir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -73,19 +80,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart=static",
            "-Xcompiler", "-fPIC", *objs, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     for o in objs:
         os.remove(o)
     with open(stamp_path, "w") as f:
         f.write(stamp + "\n")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

@@ -14,7 +14,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpsn_b200.so")
+LIB_PATH = os.environ.get("PSN_B200_LIB") or os.path.join(_HERE, "_lib", "libpsn_b200.so")  # PSN_B200_LIB: profiling builds (scripts/)
 
 PSN_OK, PSN_ERR_INVALID, PSN_ERR_DTYPE, PSN_ERR_ORDER, PSN_ERR_CUDA, PSN_ERR_ALIGN = range(6)
 PSN_F32, PSN_BF16, PSN_F64, PSN_I32 = range(4)

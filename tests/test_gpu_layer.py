@@ -177,3 +177,37 @@ def test_input_validation_errors():
         layer(torch.randn(5, 4, device="cuda"), P.Mode.TRAIN)  # rank 2
     with pytest.raises(ValueError):
         layer(torch.randn(5, 2, 4), P.Mode.TRAIN)  # CPU tensor: no CPU fallback
+
+
+@pytest.mark.parametrize("k,d", [(4, 2), (3, 1)])
+def test_exact_threshold_ties_are_bit_exact(k, d):
+    """Membranes exactly at / next to the threshold: integer inputs, running-stat
+    fusion (b_f = beta exactly) and beta in {0, +-1e-45, -1e-46}.  The streamed
+    forward decides spikes with an f32 filter and falls back to the exact f64
+    membrane on ambiguous rows; every spike must equal the reference's, ties
+    included (f32(h) >= 0, so h = -1e-46 spikes and h = -1e-45 does not)."""
+    P = _P()
+    T, N, C = 300, 20, 64
+    rng = np.random.default_rng(7 + k)
+    x_np = rng.integers(-2, 3, size=(T, N, C)).astype(np.float32)
+    x_np[:, :, 48:] = 0.0  # whole streams at h2 = b_f
+    dy_np = rng.standard_normal((T, N, C)).astype(np.float32)
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(k), device="cuda",
+                           fuse_from_batch_stats=False)
+    betas = np.array([0.0, -1e-45, -1e-46, 1e-45, 0.25, -0.25, 0.0, -1e-45] * (C // 8))
+    with torch.no_grad():
+        layer.beta.copy_(torch.tensor(betas, dtype=torch.float64))
+    p = O.init_layer(C, k, d, weight_init="uniform", rng=np.random.default_rng(k), fuse_from_batch_stats=False)
+    p.W = layer.W.detach().cpu().numpy().copy()
+    p.beta = betas.copy()
+    x = torch.tensor(x_np, device="cuda", requires_grad=True)
+    out = layer(x, P.Mode.TRAIN)
+    out.backward(torch.tensor(dy_np, device="cuda"))
+    torch.cuda.synchronize()
+    ref_out, cache, dx, dW, dg, db = O.train_step(p, x_np, dy_np)
+    got = out.detach().cpu().numpy()
+    assert np.array_equal(got, ref_out), f"{int((got != ref_out).sum())} spike mismatches at exact ties"
+    assert_close_scaled(x.grad.cpu().numpy(), dx, 1e-5, "dx")
+    assert_close_scaled(layer.W.grad.cpu().numpy(), dW, 1e-5, "dW")
+    assert_close_scaled(layer.beta.grad.cpu().numpy(), db, 1e-5, "dbeta")
