@@ -102,7 +102,7 @@ struct Args {
   double* dbeta;
   double* acc;            // [G][NV][32] per-channel pass-1 sums (f64 atomic adds, zeroed per launch)
   unsigned* cnt;          // [G] pass-1 arrivals (every CTA arrives once per group)
-  double* acc2;           // [G][2k][32] backward pass-2 BN-term sums sx, sxc (f64 atomic adds, zeroed)
+  double* acc2;           // [G][k][32] backward pass-2 BN-term sums (f64 atomic adds, zeroed)
   unsigned* cnt2;         // [G] backward pass-2 arrivals
   int flags;
   int shared;
@@ -150,15 +150,26 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
       : "memory");
   return ok != 0;
 }
-// waiting warps back off with nanosleep so they do not steal issue slots from
-// the warps doing arithmetic (latency-tolerant roles sleep longer)
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware
+// until the phase completes (or the hint expires), so waiting warps do not
+// steal issue slots from the warps doing arithmetic; the watchdog clock is
+// read only once per 64 unsuccessful polls
+__device__ __forceinline__ bool mbar_try_hint(uint64_t* b, unsigned parity, unsigned hint_ns) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
 template <unsigned SLEEP_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   if (mbar_try(b, parity)) return;
   const unsigned long long t0 = gtimer();
-  while (!mbar_try(b, parity)) {
-    if (SLEEP_NS) __nanosleep(SLEEP_NS);
-    if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired("mbarrier", (int)parity, 0);
+  for (unsigned n = 1;; ++n) {
+    if (mbar_try_hint(b, parity, 20000u)) return;
+    if ((n & 63u) == 0 && gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired("mbarrier", (int)parity, 0);
   }
 }
 
@@ -289,7 +300,7 @@ __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
   L.NV = bwd ? 1 + k : 2;   // pass-1 sums: fwd S1, S2; bwd db, dw_q[k]
-  L.NV2 = bwd ? 2 * k : 0;  // backward pass-2 BN-term sums: sx[k], sxc[k]
+  L.NV2 = bwd ? k : 0;  // backward pass-2 BN-term sums sum_t x[t-off_i] dh1[t]
   L.TB = tile_rows(es, bwd);
   L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
@@ -463,13 +474,9 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       alpha1 = dmu / m;
       beta1 = (2.0 / m) * dvar;
     }
-    if (sxs != nullptr) {  // kernel tail: dW with the BN term from the pass-2 sums sx, sxc
+    if (sxs != nullptr) {  // kernel tail: dW plus the BN term sum_t x[t-off_i] dh1[t] of pass 2
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double dw = aa * dwf[i];
-        if (flags & PSN_USE_BATCH_STATS) dw += alpha1 * sxs[i] + beta1 * sxs[K + i];  // network.py:298-315
-        a.dW[(size_t)c * K + i] = dw;
-      }
+      for (int i = 0; i < K; ++i) a.dW[(size_t)c * K + i] = aa * dwf[i] + sxs[i];  // network.py:298-315
       return;
     }
     if (store) {
@@ -729,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(p2f + sl);
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
     }
-    if constexpr (BWD) {  // dW once every CTA streamed the group's pass 2 (BN-term sums sx, sxc)
+    if constexpr (BWD) {  // dW once every CTA streamed the group's pass 2 (BN-term sums)
       for (int g = 0; g < p.G; ++g) {
         if (designated_of(p, g) != (int)blockIdx.x) continue;
         const int c = g * kCols + lane;
@@ -738,11 +745,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)p.nCTA, "pass-2 sums");
         __syncwarp();
         if (c < p.C) {
-          double tt[NV], sxs[2 * K];
+          double tt[NV], sxs[K];
 #pragma unroll
           for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
 #pragma unroll
-          for (int i = 0; i < 2 * K; ++i) sxs[i] = __ldcg(a.acc2 + ((size_t)g * 2 * K + i) * kCols + lane);
+          for (int i = 0; i < K; ++i) sxs[i] = __ldcg(a.acc2 + ((size_t)g * K + i) * kCols + lane);
           fold_channel<K, BWD>(a, c, in, tt, 0.0, 0.0, true, nullptr, sxs);
         }
       }
@@ -762,11 +769,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   int q = 0, nd = 0, cs = 0;
   unsigned cph = 0;  // parity of the current pass over the ring
   unsigned long long tc_start = gtimer(), tc_full = 0, tc_param = 0, tc_dep = 0;
+  unsigned long long tc_pass[2] = {0, 0}, tc_fullp[2] = {0, 0}, tc_t = 0;
+  int tc_cur = 0;
   const uint32_t sbase = su32(smem) + (uint32_t)((n_in * kCols + lane) * sizeof(IO));  // this thread's column
   auto wait_item = [&]() -> uint32_t {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     mbar_wait<32>(full + cs, cph);
-    if (PSN_TRACE_BUILD && a.trace) tc_full += gtimer() - t0;
+    if (PSN_TRACE_BUILD && a.trace) {
+      const unsigned long long dt = gtimer() - t0;
+      tc_full += dt;
+      tc_fullp[tc_cur] += dt;
+    }
     return sbase + (uint32_t)(cs * C_::STAGE);
   };
   auto release_item = [&]() {
@@ -846,6 +859,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int it = 0; it < iters; ++it) {
     // ------------------------------------------------------------- pass 1
     if (it < p.G) {
+      if (PSN_TRACE_BUILD && a.trace) {
+        tc_cur = 0;
+        tc_t = gtimer();
+      }
       const int g = it;
       const int v = worker_of(p, g, 0);
       const int col = g * kCols + lane;
@@ -930,7 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- backward pass 1: db, dw_q -- f64 end to end (h2 exact and f32-rounded like the
         // reference's carrier, sigma' and dh2 in f64): f32 per-element errors (~1e-7) would
         // grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5 bound on small dW
-        // entries.  The BN-term sums come from the forward (fold row sx / sxh).  Rows
+        // entries.  (The BN term of dW is summed in pass 2.)  Rows
         // alternate between two f64 accumulator sets (ILP).
         double wq[K], xd[H + U], acc2[1 + K];
 #pragma unroll
@@ -999,9 +1016,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
       }
       if (v < p.P) deposit(acc, NV);  // CTA reduction + publication happen on the publisher warp
+      if (PSN_TRACE_BUILD && a.trace) tc_pass[0] += gtimer() - tc_t;
     }
     // ------------------------------------------------------------- pass 2
     if (it >= p.lag && it - p.lag < p.G) {
+      if (PSN_TRACE_BUILD && a.trace) {
+        tc_cur = 1;
+        tc_t = gtimer();
+      }
       const int g = it - p.lag;
       const int v = worker_of(p, g, 1);
       const unsigned char* pr = take_params(g);
@@ -1077,10 +1099,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
         // partial dx of row t_blk - H + j; after a block of U rows the first U slots
-        // are complete)
+        // are complete).  Also forms the BN term of dW (network.py:298-315),
+        // sum_t x[t-off_i] dh1[t], f32 per tile and f64 across tiles.
         float w[K], wq[K], xw[H + U], pacc[H + U];
         const double* pd = (const double*)pr;
         const float* pf = (const float*)(pr + 8 * (K + 1));
+        // surrogate.py: sigma'(h) = scale / (1 + cc h^2), cc = (pi alpha / 2)^2 (arctan) or
+        // alpha (rational); the scale is folded into the w_q taps of the scatter
+        const float cc = a.sur.kind == PSN_ARCTAN ? a.sur.c * a.sur.c : a.sur.c;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           wq[i] = (float)ldsd(pd + i);
@@ -1088,6 +1114,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float bf = (float)ldsd(pd + K);
         const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);
+        float wqs[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) wqs[i] = wq[i] * a.sur.scale;
         done_params(g);
         int run_t0 = 0;
         bool lv = false;
@@ -1095,29 +1124,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto emit = [&](int od, float val) {
           if (lv && od >= run_t0 && od < p.T) st_out(out + (obase + (uint32_t)od * rs32), val, pol_out);
         };
-        // BN-term sums of this range (network.py:298-315): sx[i] = sum_t x[t-off_i],
-        // sxc[i] = sum_t x[t-off_i] (h1[t] - mu*); f32 per tile, f64 across tiles
         double sacc[kMaxNV];
 #pragma unroll
         for (int i = 0; i < kMaxNV; ++i) sacc[i] = 0.0;
-        float fsx[K], fsc[K];
+        float fsd[K];
+        // dh2 / scale and dh1 of row u of the window (rows with !ok contribute nothing)
         auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1, bool sum) {
-          float h1 = w[0] * xw[u + slot<K, D>(0)], h2 = wq[0] * xw[u + slot<K, D>(0)];
+          float h1c = fmaf(w[0], xw[u + slot<K, D>(0)], -mu), h2 = fmaf(wq[0], xw[u + slot<K, D>(0)], bf);
 #pragma unroll
           for (int i = 1; i < K; ++i) {
-            h1 = fmaf(w[i], xw[u + slot<K, D>(i)], h1);
+            h1c = fmaf(w[i], xw[u + slot<K, D>(i)], h1c);
             h2 = fmaf(wq[i], xw[u + slot<K, D>(i)], h2);
           }
-          h2 += bf;
-          const float hc = h1 - mu;
-          dh2 = ok ? yv * surrogate_grad(a.sur, h2) : 0.f;
-          dh1 = ok ? fmaf(b1, hc, a1) : 0.f;
-          if (sum && ok) {
+          const float r = rcp_approx(fmaf(cc * h2, h2, 1.0f));
+          dh2 = ok ? yv * r : 0.f;
+          dh1 = ok ? fmaf(b1, h1c, a1) : 0.f;
+          if (sum) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              fsx[i] += xw[u + slot<K, D>(i)];
-              fsc[i] = fmaf(xw[u + slot<K, D>(i)], hc, fsc[i]);
-            }
+            for (int i = 0; i < K; ++i) fsd[i] = fmaf(xw[u + slot<K, D>(i)], dh1, fsd[i]);
+          }
+        };
+        auto scatter = [&](int u, float dh2, float dh1) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            pacc[u + slot<K, D>(i)] = fmaf(wqs[i], dh2, pacc[u + slot<K, D>(i)]);
+            pacc[u + slot<K, D>(i)] = fmaf(w[i], dh1, pacc[u + slot<K, D>(i)]);
           }
         };
         // single-row step (TAIL rows): scatter, emit the row H behind, shift by one
@@ -1125,11 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           xw[H] = xv;
           float dh2, dh1;
           dh_row(0, yv, ok, dh2, dh1, false);  // TAIL rows belong to the next range's sums
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            pacc[slot<K, D>(i)] = fmaf(wq[i], dh2, pacc[slot<K, D>(i)]);
-            pacc[slot<K, D>(i)] = fmaf(w[i], dh1, pacc[slot<K, D>(i)]);
-          }
+          scatter(0, dh2, dh1);
           emit(tcur - H, pacc[0]);
 #pragma unroll
           for (int j = 0; j < H + U - 1; ++j) pacc[j] = pacc[j + 1];
@@ -1182,17 +1209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u)
                   dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u], true);
 #pragma unroll
-                for (int u = 0; u < U; ++u)
+                for (int u = 0; u < U; ++u) scatter(u, dh2[u], dh1[u]);
+                const int od0 = t0 + r0 - H;  // rows od0 .. od0+U-1 are complete now
+                if (FULL && lv && od0 >= run_t0) {  // the common case: no per-row predicate
+                  IO* op = out + (obase + (uint32_t)od0 * rs32);
 #pragma unroll
-                  for (int i = 0; i < K; ++i) {
-                    pacc[u + slot<K, D>(i)] = fmaf(wq[i], dh2[u], pacc[u + slot<K, D>(i)]);
-                    pacc[u + slot<K, D>(i)] = fmaf(w[i], dh1[u], pacc[u + slot<K, D>(i)]);
+                  for (int u = 0; u < U; ++u) {
+                    st_out(op, pacc[u], pol_out);
+                    op += rowstride;
                   }
+                } else {
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                  const int od = t0 + r0 + u - H;  // complete now
-                  const bool ok = lv && od >= run_t0 && (FULL || od < p.T);  // rows < run_t0: previous range
-                  if (ok) st_out(out + (obase + (uint32_t)od * rs32), pacc[u], pol_out);
+                  for (int u = 0; u < U; ++u) {
+                    const int od = od0 + u;
+                    const bool ok = lv && od >= run_t0 && (FULL || od < p.T);  // rows < run_t0: previous range
+                    if (ok) st_out(out + (obase + (uint32_t)od * rs32), pacc[u], pol_out);
+                  }
                 }
 #pragma unroll
                 for (int j = 0; j < H; ++j) {
@@ -1204,13 +1236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             };
 #pragma unroll
-            for (int i = 0; i < K; ++i) fsx[i] = fsc[i] = 0.f;
+            for (int i = 0; i < K; ++i) fsd[i] = 0.f;
             if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-              sacc[i] += (double)fsx[i];
-              sacc[K + i] += (double)fsc[i];
-            }
+            for (int i = 0; i < K; ++i) sacc[i] += (double)fsd[i];
           }
           release_item();
           if constexpr (H > 0) {
@@ -1234,13 +1263,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
-        if (v < p.P && !(a.ablate & 16)) deposit(sacc, 2 * K);
+        if (v < p.P && !(a.ablate & 16)) deposit(sacc, K);
       }
+      if (PSN_TRACE_BUILD && a.trace) tc_pass[1] += gtimer() - tc_t;
     }
   }
   if (PSN_TRACE_BUILD && a.trace && threadIdx.x == 0)
-    printf("PSNTRACE %s cons cta %d total %llu full %llu param %llu dep %llu items %d\n", BWD ? "bwd" : "fwd",
-           (int)blockIdx.x, gtimer() - tc_start, tc_full, tc_param, tc_dep, q);
+    printf("PSNTRACE %s cons cta %d total %llu full %llu param %llu dep %llu pass1 %llu pass2 %llu full1 %llu full2 %llu items %d\n",
+           BWD ? "bwd" : "fwd", (int)blockIdx.x, gtimer() - tc_start, tc_full, tc_param, tc_dep, tc_pass[0], tc_pass[1],
+           tc_fullp[0], tc_fullp[1], q);
 }
 
 // -------------------------------------------------------------------------
