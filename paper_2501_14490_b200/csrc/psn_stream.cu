@@ -71,10 +71,27 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   if (tpg * (long long)(g_sms + 1) >= (1LL << 32)) return false;  // 32-bit schedule arithmetic
   p.tpg = (int)tpg;
   p.nCTA = g_sms;
-  p.P = p.tpg < p.nCTA ? p.tpg : p.nCTA;
   p.lag = env_int("PSN_LAG", 2);
-  if (p.lag < 2) p.lag = 2;  // the publisher stages pass-2 parameters one iteration ahead
-  if (p.lag > 6) p.lag = 6;  // its ring of pre-update running statistics holds 8 groups
+  if (p.lag < 1) p.lag = 1;
+  if (p.lag > 6) p.lag = 6;  // the publisher's ring of pre-update running statistics holds 8 groups
+  // CTA teams: nT teams stream nT groups concurrently, so each CTA's range of a
+  // group spans several tiles (per-range costs -- HEAD rows, schedule, deposit,
+  // parameter hand-off -- amortise) while the groups whose pass 1 is resident in
+  // L2 awaiting pass 2, nT * (lag + 1) of them, still fit the L2 budget
+  {
+    const double gbytes = (double)p.T * p.N * kCols * es * (bwd ? 2 : 1);
+    const double l2_budget = 96.0 * 1024 * 1024;
+    int by_l2 = (int)(l2_budget / (gbytes * (p.lag + 1)));
+    int by_tiles = (int)((4LL * p.nCTA + p.tpg - 1) / p.tpg);  // aim at >= 4 tiles per range
+    int nT = by_l2 < by_tiles ? by_l2 : by_tiles;
+    if (nT > p.G) nT = p.G;
+    if (nT < 1) nT = 1;
+    nT = env_int("PSN_TEAMS", nT);
+    if (nT < 1) nT = 1;
+    if (nT > p.G) nT = p.G;
+    if (nT > p.nCTA) nT = p.nCTA;
+    p.nT = nT;
+  }
   p.stage_bytes = L.stage;
   const int budget = (g_smem_optin > 0 ? g_smem_optin : 232448) - L.fixed - 2048;
   int S = budget / p.stage_bytes;

@@ -81,8 +81,8 @@ struct Plan {
   int nbk;         // ceil(N / 8)
   int ttl;         // ceil(T / TB)
   int tpg;         // tiles per group = nbk * ttl
-  int P;           // workers per (pass, group) = min(nCTA, tpg)
   int nCTA;
+  int nT;          // CTA teams: team q = CTAs b with b % nT == q streams groups g with g % nT == q
   int lag;         // pass2 runs `lag` iterations behind pass1 (>= 1)
   int S;           // pipeline stages
   int stage_bytes;
@@ -339,14 +339,31 @@ __device__ __forceinline__ constexpr int slot(int i) {
 // 32-bit schedule arithmetic only (a 64-bit divide is a ~100-instruction
 // subroutine, and every warp evaluates these once per segment); the planner
 // guarantees tpg * nCTA < 2^32
-__device__ __forceinline__ int worker_of(const Plan& p, int g, int pass) {
-  const unsigned n = (unsigned)p.nCTA;
-  const unsigned rot = ((unsigned)g * 61u + (unsigned)pass * 29u) % n;
-  return (int)(((unsigned)blockIdx.x + n - rot) % n);
+// This CTA's team: member m of sz CTAs, streaming the team's ng groups
+// g = q + j * nT (j = the team-local group index); P = workers per group.
+struct Team {
+  int q, m, sz, ng, P;
+};
+__device__ __forceinline__ Team team_of(const Plan& p) {
+  Team t;
+  const unsigned nT = (unsigned)p.nT;
+  t.q = (int)(blockIdx.x % nT);
+  t.m = (int)(blockIdx.x / nT);
+  t.sz = (int)(((unsigned)p.nCTA - (unsigned)t.q + nT - 1u) / nT);
+  t.ng = p.G > t.q ? (int)(((unsigned)(p.G - t.q) + nT - 1u) / nT) : 0;
+  t.P = p.tpg < t.sz ? p.tpg : t.sz;
+  return t;
 }
-__device__ __forceinline__ void tile_range(const Plan& p, int v, int& ta, int& tb) {
-  ta = (int)((unsigned)v * (unsigned)p.tpg / (unsigned)p.P);
-  tb = (int)((unsigned)(v + 1) * (unsigned)p.tpg / (unsigned)p.P);
+// worker index of this CTA for local group j (rotated per group and pass, so
+// the idle members and the short ranges move around the team)
+__device__ __forceinline__ int worker_of(const Team& t, int j, int pass) {
+  const unsigned n = (unsigned)t.sz;
+  const unsigned rot = ((unsigned)j * 61u + (unsigned)pass * 29u) % n;
+  return (int)(((unsigned)t.m + n - rot) % n);
+}
+__device__ __forceinline__ void tile_range(const Plan& p, const Team& t, int v, int& ta, int& tb) {
+  ta = (int)((unsigned)v * (unsigned)p.tpg / (unsigned)t.P);
+  tb = (int)((unsigned)(v + 1) * (unsigned)p.tpg / (unsigned)t.P);
 }
 
 enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
@@ -495,7 +512,10 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
   }
 }
 
-__device__ __forceinline__ int designated_of(const Plan& p, int g) { return (int)(((unsigned)g * 37u + 11u) % (unsigned)p.nCTA); }
+// the team member that writes the layer outputs of local group j
+__device__ __forceinline__ bool designated(const Team& t, int j) {
+  return (int)(((unsigned)j * 37u + 11u) % (unsigned)t.sz) == t.m;
+}
 
 __device__ __forceinline__ void red_add_f64(double* a, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
@@ -547,7 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  const int iters = p.G + p.lag;
+  const Team tm = team_of(p);
+  const int iters = tm.ng > 0 ? tm.ng + p.lag : 0;
+  auto gid = [&](int j) { return tm.q + j * p.nT; };  // team-local group index -> group
 
   if (warp == kConsumerWarps) {
     // ======================= producer warp: TMA only =======================
@@ -591,12 +613,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int it = 0; it < iters; ++it) {
         for (int pass = 0; pass < 2; ++pass) {
-          const int g = pass == 0 ? it : it - p.lag;
-          if (g < 0 || g >= p.G) continue;
-          const int v = worker_of(p, g, pass);
-          if (v >= p.P) continue;
+          const int j = pass == 0 ? it : it - p.lag;
+          if (j < 0 || j >= tm.ng) continue;
+          const int g = gid(j);
+          const int v = worker_of(tm, j, pass);
+          if (v >= tm.P) continue;
           int t_a, t_b;
-          tile_range(p, v, t_a, t_b);
+          tile_range(p, tm, v, t_a, t_b);
           int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -637,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       nrm = c < p.C ? __ldcg(a.rm + c) : 0.0;
       nrv = c < p.C ? __ldcg(a.rv + c) : 0.0;
     };
-    if (!BWD && p.G > 0) prefetch_stats(0);
+    if (!BWD && tm.ng > 0) prefetch_stats(gid(0));
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
       const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
       if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
@@ -657,24 +680,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++nd;
     };
     for (int it = 0; it < iters; ++it) {
-      const bool p1 = it < p.G;
-      const int g2 = it - p.lag;
-      const bool p2 = BWD && g2 >= 0 && g2 < p.G;  // backward pass-2 BN-term sums of group it - lag
+      const bool p1 = it < tm.ng;
+      const int j2 = it - p.lag;
+      const bool p2 = BWD && j2 >= 0 && j2 < tm.ng;  // backward pass-2 BN-term sums of local group it - lag
+      const int g1 = gid(it), g2 = gid(j2);
       if (p1) {
         if (!BWD) {
           prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
           prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
-          if (it + 1 < p.G) prefetch_stats(it + 1);
+          if (it + 1 < tm.ng) prefetch_stats(gid(it + 1));
         }
-        if (worker_of(p, it, 0) < p.P) {
+        if (worker_of(tm, it, 0) < tm.P) {
           double t[kMaxNV];
           take_deposit(NV, t);
 #pragma unroll
-          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)it * NV + val) * kCols + lane, t[val]);
+          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)g1 * NV + val) * kCols + lane, t[val]);
         }
       }
       if constexpr (BWD) {
-        if (p2 && worker_of(p, g2, 1) < p.P && !(a.ablate & 16)) {
+        if (p2 && worker_of(tm, j2, 1) < tm.P && !(a.ablate & 16)) {
           double t[kMaxNV];
           take_deposit(LY.NV2, t);
 #pragma unroll
@@ -686,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0 && (p1 || p2)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (p1) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + it) : "memory");
+        if (p1) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + g1) : "memory");
         if (p2) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt2 + g2) : "memory");
       }
     }
@@ -702,30 +726,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     // arrived on the group counter, fold the group's 32 channels (lane =
     // channel) into the pass-2 parameter slot the consumers read.
     unsigned long long tf_start = gtimer(), tf_cnt = 0, tf_fold = 0;
-    for (int g = 0; g < p.G; ++g) {
-      const int sl = g & 1;
+    for (int j = 0; j < tm.ng; ++j) {
+      const int g = gid(j);
+      const int sl = j & 1;
       const int c = g * kCols + lane;
       FoldIn<K, BWD> in;
       if (c < p.C) load_fold_in<K, BWD>(a, c, in);
       unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)p.nCTA, "pass-1 sums");
+      if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)tm.sz, "pass-1 sums");
       __syncwarp();
       if (PSN_TRACE_BUILD && a.trace) {
         const unsigned long long t1 = gtimer();
         tf_cnt += t1 - t0;
         t0 = t1;
       }
-      if (g >= 2) {
-        if (lane == 0) mbar_wait<256>(p2e + sl, (unsigned)(((g >> 1) - 1) & 1));
+      if (j >= 2) {
+        if (lane == 0) mbar_wait<256>(p2e + sl, (unsigned)(((j >> 1) - 1) & 1));
         __syncwarp();
       }
       if (c < p.C) {
         double tt[NV];
 #pragma unroll
         for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
-        const double rmp = BWD ? 0.0 : prev[((g & 7) * 2 + 0) * kCols + lane];
-        const double rvp = BWD ? 0.0 : prev[((g & 7) * 2 + 1) * kCols + lane];
-        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, designated_of(p, g) == (int)blockIdx.x,
+        const double rmp = BWD ? 0.0 : prev[((j & 7) * 2 + 0) * kCols + lane];
+        const double rvp = BWD ? 0.0 : prev[((j & 7) * 2 + 1) * kCols + lane];
+        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, designated(tm, j),
                              p2s + sl * LY.pbytes + lane * LY.pstride);
       } else {
         double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
@@ -737,12 +762,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
     }
     if constexpr (BWD) {  // dW once every CTA streamed the group's pass 2 (BN-term sums)
-      for (int g = 0; g < p.G; ++g) {
-        if (designated_of(p, g) != (int)blockIdx.x) continue;
+      for (int j = 0; j < tm.ng; ++j) {
+        if (!designated(tm, j)) continue;
+        const int g = gid(j);
         const int c = g * kCols + lane;
         FoldIn<K, BWD> in;
         if (c < p.C) load_fold_in<K, BWD>(a, c, in);
-        if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)p.nCTA, "pass-2 sums");
+        if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)tm.sz, "pass-2 sums");
         __syncwarp();
         if (c < p.C) {
           double tt[NV], sxs[K];
@@ -791,16 +817,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       cph ^= 1u;
     }
   };
-  auto take_params = [&](int g) -> const unsigned char* {
-    const int sl = g & 1;
+  auto take_params = [&](int j) -> const unsigned char* {  // j: team-local group index
+    const int sl = j & 1;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait<64>(p2f + sl, (unsigned)((g >> 1) & 1));
+    mbar_wait<64>(p2f + sl, (unsigned)((j >> 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
     return p2s + sl * LY.pbytes + lane * LY.pstride;
   };
-  auto done_params = [&](int g) {
+  auto done_params = [&](int j) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(p2e + (g & 1));
+    if (lane == 0) mbar_arrive(p2e + (j & 1));
   };
   // per-warp pass-1 sums handed to the publisher: warps w and w + 8 share slot w
   // (the low warp stores, the high warp adds in fixed order and arrives)
@@ -854,21 +880,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       np1f[K] = cv ? (float)__ldg(f + 0) : 0.0f;  // mu*
     }
   };
-  if (p.G > 0) prefetch_p1(0);
+  if (tm.ng > 0) prefetch_p1(gid(0));
 
   for (int it = 0; it < iters; ++it) {
     // ------------------------------------------------------------- pass 1
-    if (it < p.G) {
+    if (it < tm.ng) {
       if (PSN_TRACE_BUILD && a.trace) {
         tc_cur = 0;
         tc_t = gtimer();
       }
-      const int g = it;
-      const int v = worker_of(p, g, 0);
+      const int g = gid(it);
+      const int v = worker_of(tm, it, 0);
       const int col = g * kCols + lane;
       int t_a, t_b;
-      tile_range(p, v, t_a, t_b);
-      if (v >= p.P) t_a = t_b = 0;
+      tile_range(p, tm, v, t_a, t_b);
+      if (v >= tm.P) t_a = t_b = 0;
       double acc[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) acc[u] = 0.0;
@@ -878,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < K; ++i) w[i] = np1d[i];
         const double sh = np1d[K];
-        if (g + 1 < p.G) prefetch_p1(g + 1);
+        if (it + 1 < tm.ng) prefetch_p1(gid(it + 1));
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -955,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < K; ++i) wq[i] = np1d[i];
         const double bf = np1d[K];
-        if (g + 1 < p.G) prefetch_p1(g + 1);
+        if (it + 1 < tm.ng) prefetch_p1(gid(it + 1));
         int tt = t_a % p.ttl;
         opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
@@ -1015,22 +1041,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
       }
-      if (v < p.P) deposit(acc, NV);  // CTA reduction + publication happen on the publisher warp
+      if (v < tm.P) deposit(acc, NV);  // CTA reduction + publication happen on the publisher warp
       if (PSN_TRACE_BUILD && a.trace) tc_pass[0] += gtimer() - tc_t;
     }
     // ------------------------------------------------------------- pass 2
-    if (it >= p.lag && it - p.lag < p.G) {
+    if (it >= p.lag && it - p.lag < tm.ng) {
       if (PSN_TRACE_BUILD && a.trace) {
         tc_cur = 1;
         tc_t = gtimer();
       }
-      const int g = it - p.lag;
-      const int v = worker_of(p, g, 1);
-      const unsigned char* pr = take_params(g);
+      const int j = it - p.lag;
+      const int g = gid(j);
+      const int v = worker_of(tm, j, 1);
+      const unsigned char* pr = take_params(j);
       const int col = g * kCols + lane;
       int t_a, t_b;
-      tile_range(p, v, t_a, t_b);
-      if (v >= p.P) t_a = t_b = 0;
+      tile_range(p, tm, v, t_a, t_b);
+      if (v >= tm.P) t_a = t_b = 0;
       IO* out = (IO*)a.out;
       if constexpr (!BWD) {
         // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
@@ -1039,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
         const double bf = ldsd(pd + K);
-        done_params(g);
+        done_params(j);
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -1117,7 +1144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float wqs[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) wqs[i] = wq[i] * a.sur.scale;
-        done_params(g);
+        done_params(j);
         int run_t0 = 0;
         bool lv = false;
         uint32_t obase = 0;
@@ -1263,7 +1290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
-        if (v < p.P && !(a.ablate & 16)) deposit(sacc, K);
+        if (v < tm.P && !(a.ablate & 16)) deposit(sacc, K);
       }
       if (PSN_TRACE_BUILD && a.trace) tc_pass[1] += gtimer() - tc_t;
     }

@@ -211,3 +211,13 @@ def test_exact_threshold_ties_are_bit_exact(k, d):
     assert_close_scaled(x.grad.cpu().numpy(), dx, 1e-5, "dx")
     assert_close_scaled(layer.W.grad.cpu().numpy(), dW, 1e-5, "dW")
     assert_close_scaled(layer.beta.grad.cpu().numpy(), db, 1e-5, "dbeta")
+
+
+@pytest.mark.parametrize("teams,lag", [(2, 1), (3, 2), (5, 3), (10, 1)])
+def test_cta_teams_and_lag_parity(monkeypatch, teams, lag):
+    """Streamed schedule variants: nT CTA teams (uneven team sizes for 3 and 5 over
+    148 SMs, one group per team for 10) and pipeline lags 1..3 give the same
+    results as the reference."""
+    monkeypatch.setenv("PSN_TEAMS", str(teams))
+    monkeypatch.setenv("PSN_LAG", str(lag))
+    _oracle_subset_check(400, 24, 320, 4, 2, channels=[0, 33, 97, 160, 255, 319], seed=teams * 10 + lag)
