@@ -75,17 +75,16 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   if (p.lag < 1) p.lag = 1;
   if (p.lag > 6) p.lag = 6;  // the publisher's ring of pre-update running statistics holds 8 groups
   // CTA teams: nT teams stream nT groups concurrently, so each CTA's range of a
-  // group spans several tiles (per-range costs -- HEAD rows, schedule, deposit,
-  // parameter hand-off -- amortise) while the groups whose pass 1 is resident in
-  // L2 awaiting pass 2, nT * (lag + 1) of them, still fit the L2 budget
+  // group spans several tiles and the per-range costs (HEAD rows, schedule,
+  // deposit, parameter hand-off) amortise.  Aim at >= 6 tiles per range and
+  // give every team the same number of groups (nT divides G, or nT = G).
+  // Measured at the metric shape: flat from 4 to 16 teams when balanced, 25%
+  // slower with 1 team or an unbalanced split (profiles/r1_sweep_teams.txt).
   {
-    const double gbytes = (double)p.T * p.N * kCols * es * (bwd ? 2 : 1);
-    const double l2_budget = 96.0 * 1024 * 1024;
-    int by_l2 = (int)(l2_budget / (gbytes * (p.lag + 1)));
-    int by_tiles = (int)((4LL * p.nCTA + p.tpg - 1) / p.tpg);  // aim at >= 4 tiles per range
-    int nT = by_l2 < by_tiles ? by_l2 : by_tiles;
-    if (nT > p.G) nT = p.G;
+    int nT = (int)((6LL * p.nCTA + p.tpg - 1) / p.tpg);
     if (nT < 1) nT = 1;
+    while (nT < p.G && p.G % nT != 0) ++nT;
+    if (nT > p.G) nT = p.G;
     nT = env_int("PSN_TEAMS", nT);
     if (nT < 1) nT = 1;
     if (nT > p.G) nT = p.G;
