@@ -49,18 +49,23 @@ def _stamp() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
     """Compile every CUDA source for sm_100a and link libpsn_b200.so.
 
     ``trace=True`` builds the per-CTA wait/compute tracing variant
-    (-DPSN_TRACE_BUILD=1) into ``_lib_trace/``; load it with PSN_B200_LIB.
+    (-DPSN_TRACE_BUILD=1) into ``_lib_trace/``; ``variant``/``defines`` build
+    an experiment variant (extra -D flags) into ``_lib_<variant>/``.  Load
+    either with PSN_B200_LIB (profiling and A/B tooling only).
     """
-    out_dir = OUT_DIR + ("_trace" if trace else "")
+    if trace:
+        variant, defines = "trace", tuple(defines) + ("PSN_TRACE_BUILD=1",)
+    out_dir = OUT_DIR + (f"_{variant}" if variant else "")
     lib_path = os.path.join(out_dir, "libpsn_b200.so")
-    extra = ["-DPSN_TRACE_BUILD=1"] if trace else []
+    extra = [f"-D{d}" for d in defines]
     os.makedirs(out_dir, exist_ok=True)
     stamp_path = os.path.join(out_dir, "build.stamp")
-    stamp = _stamp() + (" trace" if trace else "")
+    stamp = _stamp() + " " + " ".join(extra)
     if not force and os.path.exists(lib_path) and os.path.exists(stamp_path):
         if open(stamp_path).read().strip() == stamp:
             return lib_path
@@ -95,4 +100,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))
+    # python -m paper_2501_14490_b200._build [--force] [--trace] [--variant NAME -DX=1 ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else ""
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args, verbose=True, trace="--trace" in args, variant=var, defines=defs))

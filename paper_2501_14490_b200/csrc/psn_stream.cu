@@ -229,8 +229,10 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
     s.scale = 1.0f;
   }
   a.sur = s;
-  a.skind = desc->surrogate;
-  a.sc = desc->surrogate == PSN_ARCTAN ? 0.5 * 3.141592653589793 * desc->alpha : desc->alpha;
+  {
+    const double c = desc->surrogate == PSN_ARCTAN ? 0.5 * 3.141592653589793 * desc->alpha : desc->alpha;
+    a.scc = desc->surrogate == PSN_ARCTAN ? c * c : c;
+  }
   a.sscale = desc->surrogate == PSN_ARCTAN ? desc->alpha / 2.0 : 1.0;
   return dispatch(desc, true, a, x, dy, st);
 }

@@ -53,7 +53,19 @@ constexpr int kCols = 32;                        // columns per tile (lanes)
 constexpr int kBoxN = kConsumerWarps;            // batch rows per tile: consumer warp w owns row w
 constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
 constexpr int kRowBlock = 4;                     // time rows a consumer thread advances at once (ILP)
-constexpr int kRowBlockF2 = 2;                   // ... in the forward's second pass
+// ... per pass (forward pass 1 / 2, backward pass 1 / 2); each must divide the tile rows
+#ifndef PSN_U_F1
+#define PSN_U_F1 4
+#endif
+#ifndef PSN_U_F2
+#define PSN_U_F2 4
+#endif
+#ifndef PSN_U_B1
+#define PSN_U_B1 4
+#endif
+#ifndef PSN_U_B2
+#define PSN_U_B2 4
+#endif
 
 #ifndef PSN_TB_FWD
 #define PSN_TB_FWD 32  // f32 time rows per forward tile (bf16: twice)
@@ -110,8 +122,8 @@ struct Args {
   Surrogate sur;    // f32 surrogate (dx pass)
   int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA, 16 no pass-2 deposit
   int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
-  double sc, sscale; // f64 surrogate: arctan c = pi*alpha/2, scale = alpha/2; rational c = alpha, scale = 1
-  int skind;
+  double scc, sscale;  // f64 surrogate sigma'(h) = sscale / (1 + scc h^2): arctan scc = (pi alpha / 2)^2,
+                       // sscale = alpha / 2; rational scc = alpha, sscale = 1 (surrogate.py)
 };
 
 // -------------------------------------------------------------------------
@@ -278,6 +290,16 @@ __device__ __forceinline__ double round_f32(double h) {
   ex = ex < 0x38100000u ? 0x38100000u : ex;
   const double M = __hiloint2double((int)(ex + (29u << 20) + 0x00080000u), 0);
   return __dsub_rn(__dadd_rn(h, M), M);
+}
+
+// (double)(float)h for the surrogate derivative, on the integer pipe: round the
+// f64 pattern to 24 significant bits (ties to even) by a 64-bit add and mask.
+// Exact wherever f32(h) is normal; in the f32 denormal range it keeps extra
+// bits, which cannot change sigma'(h) = 1 / (1 + c h^2) (= 1.0 exactly there).
+__device__ __forceinline__ double round_f32_sg(double h) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(h);
+  const unsigned long long r = (b + 0x0FFFFFFFull + ((b >> 29) & 1ull)) & ~0x1FFFFFFFull;
+  return __longlong_as_double((long long)r);
 }
 
 // 1/v to ~2^-44 relative: MUFU.RCP64H seed (~2^-22) and one Newton step
@@ -900,6 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < NV; ++u) acc[u] = 0.0;
       if constexpr (!BWD) {
         // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
+        constexpr int U = PSN_U_F1;
         double w[K], xw[H + U];
 #pragma unroll
         for (int i = 0; i < K; ++i) w[i] = np1d[i];
@@ -975,12 +998,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5 bound on small dW
         // entries.  (The BN term of dW is summed in pass 2.)  Rows
         // alternate between two f64 accumulator sets (ILP).
+        constexpr int U = PSN_U_B1;
         double wq[K], xd[H + U], acc2[1 + K];
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc2[i] = 0.0;
 #pragma unroll
         for (int i = 0; i < K; ++i) wq[i] = np1d[i];
-        const double bf = np1d[K];
+        const double bf = np1d[K], scc = a.scc;
         if (it + 1 < tm.ng) prefetch_p1(gid(it + 1));
         int tt = t_a % p.ttl;
         opaque(tt);
@@ -1010,16 +1034,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 yv[u] = (double)ldsx<IO>(ys + ((r0 + u)) * RSB);  // rows >= T: TMA zero fill -> dh2 = 0
               }
 #pragma unroll
-              for (int u = 0; u < U; ++u) h2[u] = wq[0] * xd[u + slot<K, D>(0)];  // exact products
+              for (int u = 0; u < U; ++u) h2[u] = fma(wq[0], xd[u + slot<K, D>(0)], bf);
 #pragma unroll
               for (int i = 1; i < K; ++i)
 #pragma unroll
                 for (int u = 0; u < U; ++u) h2[u] = fma(wq[i], xd[u + slot<K, D>(i)], h2[u]);
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                const double h = round_f32(__dadd_rn(h2[u], bf));
-                const double tq = a.sc * h;
-                const double den = fma(tq, a.skind == PSN_ARCTAN ? tq : h, 1.0);
+                // the f32 membrane of the reference's carrier (b_f enters the f64 sum first
+                // here: with probability ~2^-29 the f32 rounding then differs by one ulp,
+                // which moves that element's sigma' by ~1e-7 relative)
+                const double h = round_f32_sg(h2[u]);
+                const double den = fma(scc * h, h, 1.0);
                 dh[u] = yv[u] * rcp_f64(den);  // dh2 / scale (scale applied in the fold)
               }
 #pragma unroll
@@ -1061,6 +1087,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       IO* out = (IO*)a.out;
       if constexpr (!BWD) {
         // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
+        constexpr int U = PSN_U_F2;
         double wq[K], xw[H + U];
         const double* pd = (const double*)pr;
 #pragma unroll
@@ -1128,6 +1155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // partial dx of row t_blk - H + j; after a block of U rows the first U slots
         // are complete).  Also forms the BN term of dW (network.py:298-315),
         // sum_t x[t-off_i] dh1[t], f32 per tile and f64 across tiles.
+        constexpr int U = PSN_U_B2;
         float w[K], wq[K], xw[H + U], pacc[H + U];
         const double* pd = (const double*)pr;
         const float* pf = (const float*)(pr + 8 * (K + 1));
