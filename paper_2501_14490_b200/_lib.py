@@ -7,6 +7,7 @@ raises for the same conditions (ValueError / TypeError; RuntimeError for CUDA).
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import threading
@@ -140,6 +141,27 @@ def stream_of(t: torch.Tensor) -> int:
 def workspace(desc: PsnDesc, device) -> torch.Tensor:
     n = lib().psn_workspace_bytes(ctypes.byref(desc))
     return torch.empty(max(int(n), 256), dtype=torch.uint8, device=device)
+
+
+_WS_CACHE: "collections.OrderedDict" = collections.OrderedDict()
+
+
+def workspace_for(desc: PsnDesc, device, stream: int) -> torch.Tensor:
+    """A persistent workspace per (device, stream, descriptor geometry).
+
+    Saves an allocation per call; the kernels need no particular content (each
+    launch zeroes its counters and accumulators)."""
+    key = (torch.device(device).index, int(stream), desc.T, desc.N, desc.C, desc.Q, desc.k, desc.d,
+           desc.dtype, desc.flags)
+    ws = _WS_CACHE.get(key)
+    if ws is None:
+        ws = workspace(desc, device)
+        _WS_CACHE[key] = ws
+        while len(_WS_CACHE) > 32:
+            _WS_CACHE.popitem(last=False)
+    else:
+        _WS_CACHE.move_to_end(key)
+    return ws
 
 
 def plan_info(desc: PsnDesc, backward: bool) -> dict:

@@ -54,7 +54,7 @@ class _PSNFunction(torch.autograd.Function):
         lib = L.lib()
         out = torch.empty_like(x)
         fold = torch.empty((x.shape[2], L.PSN_FOLD_HDR + 2 * desc.k), dtype=torch.float64, device=x.device)
-        ws = L.workspace(desc, x.device)
+        ws = L.workspace_for(desc, x.device, L.stream_of(x))
         L.check(lib.psn_forward_train(ctypes.byref(desc), L.ptr(x), L.ptr(W), L.ptr(gamma), L.ptr(beta),
                                       L.ptr(running_mean), L.ptr(running_var), L.ptr(out), L.ptr(fold),
                                       L.ptr(ws), L.stream_of(x)))
@@ -73,7 +73,7 @@ class _PSNFunction(torch.autograd.Function):
         dW = torch.empty_like(W)
         dgamma = torch.empty_like(gamma)
         dbeta = torch.empty_like(gamma)
-        ws = L.workspace(desc, x.device)
+        ws = L.workspace_for(desc, x.device, L.stream_of(x))
         L.check(L.lib().psn_backward(ctypes.byref(desc), L.ptr(x), L.ptr(dy), L.ptr(W), L.ptr(gamma),
                                      L.ptr(fold), L.ptr(dx), L.ptr(dW), L.ptr(dgamma), L.ptr(dbeta),
                                      L.ptr(ws), L.stream_of(x)))

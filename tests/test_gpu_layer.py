@@ -221,3 +221,54 @@ def test_cta_teams_and_lag_parity(monkeypatch, teams, lag):
     monkeypatch.setenv("PSN_TEAMS", str(teams))
     monkeypatch.setenv("PSN_LAG", str(lag))
     _oracle_subset_check(400, 24, 320, 4, 2, channels=[0, 33, 97, 160, 255, 319], seed=teams * 10 + lag)
+
+
+def _abi_step(P, L, x, dy, layer, desc, ws):
+    """One fwd+bwd through the C ABI on a caller-provided workspace."""
+    import ctypes
+    C, k = x.shape[2], desc.k
+    out, dx = torch.empty_like(x), torch.empty_like(x)
+    fold = torch.empty((C, L.PSN_FOLD_HDR + 2 * k), dtype=torch.float64, device=x.device)
+    dW = torch.empty((C, k), dtype=torch.float64, device=x.device)
+    dg, db = torch.empty(C, dtype=torch.float64, device=x.device), torch.empty(C, dtype=torch.float64, device=x.device)
+    rm, rv = layer.running_mean.clone(), layer.running_var.clone()
+    sp = torch.cuda.current_stream().cuda_stream
+    lib = L.lib()
+    L.check(lib.psn_forward_train(ctypes.byref(desc), x.data_ptr(), layer.W.data_ptr(), layer.gamma.data_ptr(),
+                                  layer.beta.data_ptr(), rm.data_ptr(), rv.data_ptr(), out.data_ptr(),
+                                  fold.data_ptr(), ws.data_ptr(), sp))
+    L.check(lib.psn_backward(ctypes.byref(desc), x.data_ptr(), dy.data_ptr(), layer.W.data_ptr(),
+                             layer.gamma.data_ptr(), fold.data_ptr(), dx.data_ptr(), dW.data_ptr(), dg.data_ptr(),
+                             db.data_ptr(), ws.data_ptr(), sp))
+    torch.cuda.synchronize()
+    return [t.cpu() for t in (out, dx, dW, dg, db, rm, rv)]
+
+
+def test_workspace_reuse_garbage_and_alternating_geometries():
+    """Workspace contract: any content is fine.  Repeated calls, a garbage-filled
+    buffer and a buffer alternating between two geometries must all give the
+    same results as a fresh zeroed workspace."""
+    P = _P()
+    from paper_2501_14490_b200 import _lib as L
+    shapes = [(300, 20, 128), (257, 12, 64)]
+    runs = []
+    for T, N, C in shapes:
+        cfg = P.NeuronConfig(channels=C, order=4, dilation=2, quantized=True)
+        layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(C), device="cuda")
+        x = torch.randn((T, N, C), device="cuda")
+        dy = torch.randn((T, N, C), device="cuda")
+        desc = L.make_desc(x.shape, 4, 2, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+        runs.append((x, dy, layer, desc))
+    nbytes = max(int(L.lib().psn_workspace_bytes(__import__("ctypes").byref(r[3]))) for r in runs)
+    refs = [_abi_step(P, L, x, dy, layer, desc, torch.zeros(nbytes, dtype=torch.uint8, device="cuda"))
+            for x, dy, layer, desc in runs]
+
+    def same(got, ref):
+        assert torch.equal(got[0], ref[0]), "spikes"
+        for g, r in zip(got[1:], ref[1:]):
+            torch.testing.assert_close(g, r, rtol=1e-6, atol=1e-9)
+
+    shared = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device="cuda")  # garbage
+    for rep in range(3):
+        for (x, dy, layer, desc), ref in zip(runs, refs):
+            same(_abi_step(P, L, x, dy, layer, desc, shared), ref)
