@@ -7,33 +7,35 @@
 // -> spikes from h2; backward: db/dw sums -> dx).  Streaming x (and dy) twice
 // from HBM costs 32 B/elem against the 20 B/elem algorithmic minimum (f32).
 // So the channels are cut into groups of 32 columns (one 128-byte row segment
-// per (t, n)), small enough that a group's x (+dy) stays in the 126 MB L2
-// between its two passes, and the passes are software-pipelined over groups
-// inside one cooperative launch (one CTA per SM):
+// per (t, n)) and the two passes are software-pipelined over groups inside one
+// cooperative launch (one CTA per SM):
 //
-//     iteration it:  pass1(it)  |  fold(it-1) on its folder CTAs  |  pass2(it-LAG)
+//     iteration it:  pass1(it)  |  fold(it-1) on the folder warp  |  pass2(it-LAG)
 //
-// pass1 streams group `it` from HBM (TMA, L2 evict_last) and publishes per-CTA
-// partial sums; fold(g) (tiny, fixed-order f64 sums over the per-CTA slots)
-// runs on F statically chosen folder CTAs one iteration later; pass2 re-reads
-// group it-LAG from L2 (TMA, evict_first) and writes spikes / dx.
+// pass1 streams group `it` (TMA, L2 evict_last) and publishes per-CTA partial
+// sums (f64 red.add per channel + an arrival counter); every CTA of the team
+// folds the group once all members arrived; pass2 re-reads the group (TMA,
+// evict_first) and writes spikes / dx.  The CTAs form nT teams (CTA b is in
+// team b % nT) that stream different groups concurrently, so that each CTA's
+// share of a group spans several tiles.
 //
-// Inside a CTA: warp 8 is the TMA producer (one elected lane issues
+// Inside a CTA: warp 16 is the TMA producer (one elected lane issues
 // cp.async.bulk.tensor into a ring of S stages guarded by full/empty
-// mbarriers; the warp also gathers each segment's per-channel parameters into
-// the stage), warps 0..7 consume.  A tile is a TMA box [32 columns][8 batch
-// rows][TB time steps] of the time-major tensor; lane = column (channel),
-// warp = batch row, and each thread walks its (n, c) stream down the tile
-// with a register window of the last H = (K-1)*D inputs, so every element is
-// read from shared memory once and the dilated taps are register renames.  A
-// thread keeps its window across consecutive tiles of its tile range; where a
-// range starts mid-stream a HEAD item (H rows before the tile) primes it, and
-// where the backward's dx range ends mid-stream a TAIL item (H rows after)
-// supplies the future dh the time-reversed conv needs.
+// mbarriers), warp 17 publishes the consumers' sums, warp 18 folds, warps
+// 0..15 consume.  A tile is a TMA box [32 columns][16 batch rows][TB time
+// steps] of the time-major tensor; lane = column (channel), warp = batch row,
+// and each thread walks its (n, c) stream down the tile with a register window
+// of the last H = (K-1)*D inputs, so every element is read from shared memory
+// once and the dilated taps are register renames.  A thread keeps its window
+// across consecutive tiles of its tile range; where a range starts mid-stream
+// a HEAD item (H rows before the tile) primes it, and where the backward's dx
+// range ends mid-stream a TAIL item (H rows after) supplies the future dh the
+// time-reversed conv needs.
 //
 // Work is assigned statically (contiguous tile ranges per CTA, rotated per
-// group so remainders spread), so every per-channel sum is formed in a fixed
-// order: results are bit-reproducible run to run.
+// group so remainders spread) and every CTA reduces its sums in a fixed order;
+// the cross-CTA f64 atomic adds make results reproducible to ~1 ulp of those
+// sums.
 #pragma once
 
 #include <cuda.h>
@@ -544,8 +546,8 @@ __device__ __forceinline__ void red_add_f64(double* a, double v) {
 }
 
 // -------------------------------------------------------------------------
-// the kernel: warps 0..7 consume tiles, warp 8 issues TMA, warp 9 publishes
-// partial sums, folds, and stages per-segment parameters
+// the kernel: warps 0..15 consume tiles, warp 16 issues TMA, warp 17
+// publishes the per-group sums, warp 18 folds (see the file header)
 // -------------------------------------------------------------------------
 template <int K, int D, typename IO, bool BWD>
 __global__ void __launch_bounds__(kThreads, 1)
