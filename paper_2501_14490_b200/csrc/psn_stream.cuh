@@ -685,6 +685,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       nrv = c < p.C ? __ldcg(a.rv + c) : 0.0;
     };
     if (!BWD && tm.ng > 0) prefetch_stats(gid(0));
+    // pass-1 parameters for local group j into slot j & 1 (freed by the
+    // consumers' done_p1(j - 2))
+    auto stage_p1 = [&](int j) {
+      if (j >= 2) {
+        if (lane == 0) mbar_wait<256>(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
+        __syncwarp();
+      }
+      const int c = gid(j) * kCols + lane;
+      const bool cv = c < p.C;
+      const int cc = cv ? c : 0;
+      double* d = (double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
+      if constexpr (!BWD) {
+        const double* Wc = a.W + (size_t)(a.shared ? 0 : cc) * K;
+#pragma unroll
+        for (int i = 0; i < K; ++i) d[i] = cv ? __ldg(Wc + i) : 0.0;
+        d[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments (pre-update running mean)
+      } else {
+        const double* f = a.fold + (size_t)cc * PSN_FOLD_STRIDE(K);
+#pragma unroll
+        for (int i = 0; i < K; ++i) d[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;  // w_q
+        d[K] = cv ? __ldg(f + 3) : 0.0;                                                // b_f
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p1f + (j & 1));
+    };
+    if (tm.ng > 0) stage_p1(0);
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
       const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
       if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
@@ -708,6 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j2 = it - p.lag;
       const bool p2 = BWD && j2 >= 0 && j2 < tm.ng;  // backward pass-2 BN-term sums of local group it - lag
       const int g1 = gid(it), g2 = gid(j2);
+      if (it + 1 < tm.ng) stage_p1(it + 1);
       if (p1) {
         if (!BWD) {
           prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
@@ -877,34 +904,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const size_t rowstride = (size_t)p.N * p.J;
   const uint32_t rs32 = (uint32_t)rowstride;  // the planner guarantees T*N*C < 2^32
   const unsigned mN = (unsigned)p.N;
-  // pass-1 parameters are inputs of this launch (W, running mean / the forward's
-  // fold rows), so each consumer loads its column's next segment one segment ahead
-  double np1d[K + 1];
-  float np1f[K + 1];
-  auto prefetch_p1 = [&](int g) {
-    const int c = g * kCols + lane;
-    const bool cv = c < p.C;
-    const int cc = cv ? c : 0;
-    const int wr = a.shared ? 0 : cc;
-    if constexpr (!BWD) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        np1d[i] = cv ? __ldg(a.W + (size_t)wr * K + i) : 0.0;
-        np1f[i] = (float)np1d[i];
-      }
-      np1d[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments (pre-update running mean)
-    } else {
-      const double* f = a.fold + (size_t)cc * PSN_FOLD_STRIDE(K);
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        np1d[i] = cv ? __ldg(f + PSN_FOLD_HDR + K + i) : 0.0;  // w_q
-        np1f[i] = cv ? (float)__ldg(a.W + (size_t)wr * K + i) : 0.0f;
-      }
-      np1d[K] = cv ? __ldg(f + 3) : 0.0;          // b_f
-      np1f[K] = cv ? (float)__ldg(f + 0) : 0.0f;  // mu*
-    }
+  // pass-1 parameters of local group j (W and the moment shift, or the
+  // forward's w_q and b_f): staged in shared memory by the publisher warp
+  auto take_p1 = [&](int j) -> const double* {
+    mbar_wait<64>(p1f + (j & 1), (unsigned)((j >> 1) & 1));
+    return (const double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
   };
-  if (tm.ng > 0) prefetch_p1(gid(0));
+  auto done_p1 = [&](int j) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p1e + (j & 1));
+  };
 
   for (int it = 0; it < iters; ++it) {
     // ------------------------------------------------------------- pass 1
@@ -925,11 +934,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!BWD) {
         // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
         constexpr int U = PSN_U_F1;
-        double w[K], xw[H + U];
+        double w[K], xw[H + U], sh;
 #pragma unroll
-        for (int i = 0; i < K; ++i) w[i] = np1d[i];
-        const double sh = np1d[K];
-        if (it + 1 < tm.ng) prefetch_p1(gid(it + 1));
+        {
+          const double* pp = take_p1(it);
+          for (int i = 0; i < K; ++i) w[i] = ldsd(pp + i);
+          sh = ldsd(pp + K);
+          done_p1(it);
+        }
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         opaque(nbi);
         opaque(tt);
@@ -969,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u) h[u] = fma(w[i], xw[u + slot<K, D>(i)], h[u]);
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                double hc = round_f32(h[u]) - sh;
+                double hc = round_f32_sg(h[u]) - sh;
                 if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
                 S1[u] += hc;
                 S2[u] = fma(hc, hc, S2[u]);
@@ -1005,9 +1017,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc2[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < K; ++i) wq[i] = np1d[i];
-        const double bf = np1d[K], scc = a.scc;
-        if (it + 1 < tm.ng) prefetch_p1(gid(it + 1));
+        double bf;
+        {
+          const double* pp = take_p1(it);
+          for (int i = 0; i < K; ++i) wq[i] = ldsd(pp + i);
+          bf = ldsd(pp + K);
+          done_p1(it);
+        }
+        const double scc = a.scc;
         int tt = t_a % p.ttl;
         opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
