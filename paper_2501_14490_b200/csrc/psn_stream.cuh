@@ -69,6 +69,10 @@ constexpr int kRowBlock = 4;                     // time rows a consumer thread 
 #define PSN_U_B2 4
 #endif
 
+#ifndef PSN_B1_ALT
+#define PSN_B1_ALT 1  // backward pass 1: alternate rows between two f64 accumulator sets (ILP)
+#endif
+
 #ifndef PSN_TB_FWD
 #define PSN_TB_FWD 32  // f32 time rows per forward tile (bf16: twice)
 #endif
@@ -1069,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                double* A = (u & 1) ? acc2 : acc;
+                double* A = (PSN_B1_ALT && (u & 1)) ? acc2 : acc;
                 A[0] += dh[u];
 #pragma unroll
                 for (int i = 0; i < K; ++i) A[1 + i] = fma(xd[u + slot<K, D>(i)], dh[u], A[1 + i]);
