@@ -39,3 +39,17 @@ ev[2].record()
 for _ in range(20): fwd(); bwd()
 ev[3].record(); torch.cuda.synchronize()
 print(f"direct step {ev[2].elapsed_time(ev[3])/20*1000:.1f} us")
+# isolated vs alternating launches (device time per call)
+def timed(fn_list, reps=20):
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps * len(fn_list))]
+    k = 0
+    for _ in range(reps):
+        for fn in fn_list:
+            evs[k][0].record(); fn(); evs[k][1].record(); k += 1
+    torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) * 1000 for a, b in evs]
+    return [sum(ts[i::len(fn_list)]) / reps for i in range(len(fn_list))]
+print("fwd only   %.1f us" % timed([fwd])[0])
+print("bwd only   %.1f us" % timed([bwd])[0])
+f_, b_ = timed([fwd, bwd])
+print("alternating fwd %.1f us, bwd %.1f us" % (f_, b_))
