@@ -117,12 +117,14 @@ def run_reference(args, rank: int, world: int):
     """--impl reference: the reference algorithm on the host cores, rank 0 only."""
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 5))
-    res = cpu_baseline(args, steps=steps, warmup=1 if args.warmup > 0 else 0)
+    # every step is one bounded sample (B=8 of the workload, ~40 ms on 16 cores),
+    # so the full --steps K --warmup W run stays within seconds to a minute
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    res = cpu_baseline(args, steps=steps, warmup=warmup)
     v = res.get("value")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "warmup": 1, "ms_per_step": (res.get("seconds_per_step") or 0) * 1e3,
+        "steps": steps, "warmup": warmup, "ms_per_step": (res.get("seconds_per_step") or 0) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic N(0,1) x, dy; uniform(±k^-1/2) W",
         "config": {"workload": f"SpikingLayer TRAIN fwd+bwd T={args.T},B={args.B},C={args.C},k={args.k},"
