@@ -129,7 +129,8 @@ PSN_API int psn_forward_eval(const psn_desc_t *desc, const void *x, const double
 /* Execution plan of psn_forward_train (backward = 0) / psn_backward (1):
  * info[0] = 1 if the persistent fused kernel runs (else the generic 3-kernel path),
  * info[1] = CTAs, info[2] = channel groups, info[3] = 32-column tiles per group,
- * info[4] = row slices, info[5] = kernel launches per call (memsets included).
+ * info[4] = pipeline stages, info[5] = kernel launches per call (memsets included),
+ * info[6] = CTA teams (groups streamed concurrently), info[7] = pass-2 lag in groups.
  * Returns the number of entries written (<= n).                                  */
 PSN_API int psn_plan_info(const psn_desc_t *desc, int backward, int64_t *info, int n);
 

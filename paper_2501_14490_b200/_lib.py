@@ -165,9 +165,9 @@ def workspace_for(desc: PsnDesc, device, stream: int) -> torch.Tensor:
 
 
 def plan_info(desc: PsnDesc, backward: bool) -> dict:
-    buf = (ctypes.c_int64 * 6)()
-    n = lib().psn_plan_info(ctypes.byref(desc), int(backward), buf, 6)
-    keys = ("streamed", "ctas", "groups", "tiles_per_group", "stages", "launches")
+    buf = (ctypes.c_int64 * 8)()
+    n = lib().psn_plan_info(ctypes.byref(desc), int(backward), buf, 8)
+    keys = ("streamed", "ctas", "groups", "tiles_per_group", "stages", "launches", "teams", "lag")
     return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
 
 

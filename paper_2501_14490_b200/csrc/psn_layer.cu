@@ -856,7 +856,7 @@ int psn_forward_eval(const psn_desc_t* desc, const void* x, const double* W, con
 //         kernel launches per call (memsets included)}.
 int psn_plan_info(const psn_desc_t* desc, int backward, int64_t* info, int n) {
   if (!desc || !info || n <= 0 || validate(desc, false) != PSN_OK) return 0;
-  int64_t v[6] = {0, 0, 0, 0, 0, 3};
+  int64_t v[8] = {0, 0, 0, 0, 0, 3, 0, 0};
   const int rowsum = (backward && (desc->flags & PSN_SHARED)) ? 1 : 0;
   stream::Plan P;
   if (stream::make_plan(desc, backward != 0, P)) {
@@ -866,10 +866,12 @@ int psn_plan_info(const psn_desc_t* desc, int backward, int64_t* info, int n) {
     v[3] = P.tpg;
     v[4] = P.S;
     v[5] = 2 + rowsum;
+    v[6] = P.nT;
+    v[7] = P.lag;
   } else {
     v[5] = 3 + rowsum;
   }
-  const int m = n < 6 ? n : 6;
+  const int m = n < 8 ? n : 8;
   for (int i = 0; i < m; ++i) info[i] = v[i];
   return m;
 }

@@ -53,3 +53,20 @@ print("fwd only   %.1f us" % timed([fwd])[0])
 print("bwd only   %.1f us" % timed([bwd])[0])
 f_, b_ = timed([fwd, bwd])
 print("alternating fwd %.1f us, bwd %.1f us" % (f_, b_))
+# cost of a small stream memset (what each streamed launch does first)
+import ctypes as _ct
+_cudart = _ct.CDLL("libcudart.so") if False else None
+def ms_only():
+    torch.cuda.current_stream().synchronize()
+zb = 24576
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(100):
+    ws[:zb].zero_()
+e1.record(); torch.cuda.synchronize()
+print("24 KB fill kernel: %.2f us each (back to back)" % (e0.elapsed_time(e1) * 10))
+e0.record()
+for _ in range(20):
+    ws[:zb].zero_(); fwd()
+e1.record(); torch.cuda.synchronize()
+print("fill + fwd: %.1f us" % (e0.elapsed_time(e1) * 50))
