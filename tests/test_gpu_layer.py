@@ -272,3 +272,52 @@ def test_workspace_reuse_garbage_and_alternating_geometries():
     for rep in range(3):
         for (x, dy, layer, desc), ref in zip(runs, refs):
             same(_abi_step(P, L, x, dy, layer, desc, shared), ref)
+
+
+def test_cuda_graph_capture_replays_the_step():
+    """The C-ABI calls are stream-ordered and allocation-free, so one fwd+bwd
+    step captures into a CUDA graph; replays give the direct results."""
+    import ctypes
+    P = _P()
+    from paper_2501_14490_b200 import _lib as L
+    T, N, C, k, d = 300, 20, 128, 4, 2
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(3), device="cuda")
+    x = torch.randn((T, N, C), device="cuda")
+    dy = torch.randn((T, N, C), device="cuda")
+    desc = L.make_desc(x.shape, k, d, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+    ws = L.workspace(desc, x.device)
+    out, dx = torch.empty_like(x), torch.empty_like(x)
+    fold = torch.empty((C, L.PSN_FOLD_HDR + 2 * k), dtype=torch.float64, device="cuda")
+    dW = torch.empty((C, k), dtype=torch.float64, device="cuda")
+    dg, db = torch.empty(C, dtype=torch.float64, device="cuda"), torch.empty(C, dtype=torch.float64, device="cuda")
+    rm0, rv0 = layer.running_mean.clone(), layer.running_var.clone()
+    lib = L.lib()
+
+    def step(stream):
+        L.check(lib.psn_forward_train(ctypes.byref(desc), x.data_ptr(), layer.W.data_ptr(), layer.gamma.data_ptr(),
+                                      layer.beta.data_ptr(), layer.running_mean.data_ptr(),
+                                      layer.running_var.data_ptr(), out.data_ptr(), fold.data_ptr(),
+                                      ws.data_ptr(), stream))
+        L.check(lib.psn_backward(ctypes.byref(desc), x.data_ptr(), dy.data_ptr(), layer.W.data_ptr(),
+                                 layer.gamma.data_ptr(), fold.data_ptr(), dx.data_ptr(), dW.data_ptr(),
+                                 dg.data_ptr(), db.data_ptr(), ws.data_ptr(), stream))
+
+    step(torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (out, dx, dW, dg, db)]
+    ref_stats = (layer.running_mean.clone(), layer.running_var.clone())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step(torch.cuda.current_stream().cuda_stream)
+    for t in (out, dx, dW, dg, db):
+        t.zero_()
+    layer.running_mean.copy_(rm0)
+    layer.running_var.copy_(rv0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref[0])
+    for got, want in zip((dx, dW, dg, db), ref[1:]):
+        torch.testing.assert_close(got, want, rtol=1e-6, atol=1e-9)
+    torch.testing.assert_close(layer.running_mean, ref_stats[0], rtol=1e-12, atol=0)
+    torch.testing.assert_close(layer.running_var, ref_stats[1], rtol=1e-12, atol=0)
