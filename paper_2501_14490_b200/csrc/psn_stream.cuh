@@ -181,7 +181,6 @@ __device__ __forceinline__ bool mbar_try_hint(uint64_t* b, unsigned parity, unsi
       : "memory");
   return ok != 0;
 }
-template <unsigned SLEEP_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   if (mbar_try(b, parity)) return;
   const unsigned long long t0 = gtimer();
@@ -226,9 +225,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_release(unsigned* a, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
 // one thread waits for a grid counter (co-residency is guaranteed by the
 // cooperative launch); callers publish the result with a CTA barrier
 __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target, const char* what) {
@@ -239,10 +235,6 @@ __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target,
     __nanosleep(1000);
     if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired(what, (int)v, (int)target);
   }
-}
-
-__device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 consumer warps
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 }
 
 // streaming stores of the outputs (L2 evict_first: keep the resident groups)
@@ -265,18 +257,6 @@ __device__ __forceinline__ float ldsx<__nv_bfloat16>(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return __uint_as_float(((unsigned)v) << 16);
 }
-// explicit shared-space loads (the stage pointers are computed from an aligned
-// integer, so the compiler would otherwise emit generic LD for them)
-__device__ __forceinline__ float lds(const float* p) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(su32(p)));
-  return v;
-}
-__device__ __forceinline__ float lds(const __nv_bfloat16* p) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(su32(p)));
-  return __uint_as_float(((unsigned)v) << 16);
-}
 __device__ __forceinline__ double ldsd(const double* p) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(su32(p)));
@@ -288,20 +268,12 @@ __device__ __forceinline__ float ldsf(const float* p) {
   return v;
 }
 
-// exact (double)(float)h with two DADDs (F2F.F32.F64 issues at ~8/clk/SM on
-// B200, DADD at 64): adding M = 1.5 * 2^(E+29) puts the rounding point of the
-// sum at ulp_f32(h); ties-to-even is preserved, f32 denormals included
-__device__ __forceinline__ double round_f32(double h) {
-  unsigned ex = (unsigned)__double2hiint(h) & 0x7ff00000u;
-  ex = ex < 0x38100000u ? 0x38100000u : ex;
-  const double M = __hiloint2double((int)(ex + (29u << 20) + 0x00080000u), 0);
-  return __dsub_rn(__dadd_rn(h, M), M);
-}
-
-// (double)(float)h for the surrogate derivative, on the integer pipe: round the
-// f64 pattern to 24 significant bits (ties to even) by a 64-bit add and mask.
-// Exact wherever f32(h) is normal; in the f32 denormal range it keeps extra
-// bits, which cannot change sigma'(h) = 1 / (1 + c h^2) (= 1.0 exactly there).
+// (double)(float)h on the integer pipe (F2F.F32.F64 issues at only ~8/clk/SM,
+// profiles/r1_microbench_pipes.txt): round the f64 pattern to 24 significant
+// bits (ties to even) by a 64-bit add and mask.  Exact wherever f32(h) is
+// normal.  In the f32 denormal range (|h| < 2^-126) it keeps extra bits: that
+// cannot change sigma'(h) = 1 / (1 + c h^2) (1.0 exactly there), and moves a
+// moment sum by < 2^-149 per element.
 __device__ __forceinline__ double round_f32_sg(double h) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(h);
   const unsigned long long r = (b + 0x0FFFFFFFull + ((b >> 29) & 1ull)) & ~0x1FFFFFFFull;
@@ -613,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
         if (q >= p.S) {
           const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-          mbar_wait<128>(empty + s, ph ^ 1u);
+          mbar_wait(empty + s, ph ^ 1u);
           if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
@@ -693,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // consumers' done_p1(j - 2))
     auto stage_p1 = [&](int j) {
       if (j >= 2) {
-        if (lane == 0) mbar_wait<256>(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
+        if (lane == 0) mbar_wait(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
         __syncwarp();
       }
       const int c = gid(j) * kCols + lane;
@@ -717,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tm.ng > 0) stage_p1(0);
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
       const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      if (lane == 0) mbar_wait<256>(depf, (unsigned)(nd & 1));
+      if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
       __syncwarp();
       if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
 #pragma unroll
@@ -796,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         t0 = t1;
       }
       if (j >= 2) {
-        if (lane == 0) mbar_wait<256>(p2e + sl, (unsigned)(((j >> 1) - 1) & 1));
+        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((j >> 1) - 1) & 1));
         __syncwarp();
       }
       if (c < p.C) {
@@ -855,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = su32(smem) + (uint32_t)((n_in * kCols + lane) * sizeof(IO));  // this thread's column
   auto wait_item = [&]() -> uint32_t {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait<32>(full + cs, cph);
+    mbar_wait(full + cs, cph);
     if (PSN_TRACE_BUILD && a.trace) {
       const unsigned long long dt = gtimer() - t0;
       tc_full += dt;
@@ -875,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto take_params = [&](int j) -> const unsigned char* {  // j: team-local group index
     const int sl = j & 1;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait<64>(p2f + sl, (unsigned)((j >> 1) & 1));
+    mbar_wait(p2f + sl, (unsigned)((j >> 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
     return p2s + sl * LY.pbytes + lane * LY.pstride;
   };
@@ -887,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (the low warp stores, the high warp adds in fixed order and arrives)
   auto deposit = [&](const double* acc, int nv) {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    if (nd >= 1) mbar_wait<64>(depe, (unsigned)((nd - 1) & 1));
+    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1));
     if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
     const int sw = warp & 7;
     if (warp < 8) {
@@ -911,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // pass-1 parameters of local group j (W and the moment shift, or the
   // forward's w_q and b_f): staged in shared memory by the publisher warp
   auto take_p1 = [&](int j) -> const double* {
-    mbar_wait<64>(p1f + (j & 1), (unsigned)((j >> 1) & 1));
+    mbar_wait(p1f + (j & 1), (unsigned)((j >> 1) & 1));
     return (const double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
   };
   auto done_p1 = [&](int j) {
