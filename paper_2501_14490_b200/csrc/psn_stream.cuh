@@ -126,7 +126,8 @@ struct Args {
   int shared;
   double eps, momentum;
   Surrogate sur;    // f32 surrogate (dx pass)
-  int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA, 16 no pass-2 deposit
+  int ablate;        // PSN_ABLATE (benchmarking only): 1 no row math, 2 no cross-CTA wait, 4 no TMA,
+                     // 16 no pass-2 deposit, 64 no L2 evict_last/evict_first hints
   int trace;         // PSN_TRACE: print per-CTA wait/compute breakdown at kernel end
   double scc, sscale;  // f64 surrogate sigma'(h) = sscale / (1 + scc h^2): arctan scc = (pi alpha / 2)^2,
                        // sscale = alpha / 2; rational scc = alpha, sscale = 1 (surrogate.py)
@@ -589,7 +590,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
-        const uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
+        uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
+        if (a.ablate & 64) pol = pol_norm;  // experiment: no L2 residency hints
         const int c0 = g * kCols, n0 = nbi * kBoxN;
         if (a.ablate & 4) {
           mbar_arrive(full + s);
