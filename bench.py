@@ -2,22 +2,30 @@
 SpikingLayer TRAIN forward + surrogate-gradient backward at T=1024, B=64,
 C=512 (order 4, dilation 1, fp32 I/O, quantized, batch-stat BN fusion).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--scaling strong|weak] [--impl reference]
 
-One process per GPU (torchrun for N>1, NCCL): each rank runs the layer on its
-own batch of B=64 (weak scaling) and the per-channel parameter gradients are
-all-reduced every step (DDP semantics).  Prints ONE JSON line on rank 0.
+One process per GPU, NCCL.  `--gpus N` with N > 1
+relaunches itself under torch.distributed.run when it is not already running
+under it (and exits non-zero when WORLD_SIZE disagrees with N).  Prints ONE
+JSON line on rank 0.
 
-value   : Gsteps·ch/s = ranks * T*B*C / device time per step (max over ranks),
-          inputs resident in HBM, CUDA events on the launch stream.
-e2e     : the same metric through the public module API (SpikingLayer
-          autograd) with x, dy in pinned host memory copied H2D inside the
-          timed region and the gradients read back D2H every step.
+value   : Gsteps·ch/s of the whole job = T*B*C / device time per step (max over
+          ranks), inputs resident in HBM, CUDA events on the launch stream.
+          Default `--scaling strong`: the global batch B=64 is split across the
+          ranks (ddp.shard_bounds, B=8 per GPU at N=8), as BASELINE.md section 2
+          defines the 1/2/4/8-GPU metric.  N>1 also reports the weak-scaling
+          figure (B=64 per rank) under "weak".  Every step all-reduces the
+          per-channel gradients through ddp.GradBucket (NCCL).
+e2e     : the same metric through the public module API (SpikingLayer autograd)
+          from pinned host memory: x and dy are copied H2D and the spikes, dx
+          and the gradient bucket D2H every step (copy streams overlap the
+          previous / next step's compute).
 roofline: algorithmic HBM bytes (20 B/elem fp32: fwd reads x, writes s; bwd
-          reads x, dy, writes dx) of the dominant launch group over its
-          CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
---impl reference: the reference algorithm (numpy oracle, every host core,
-          channels split across processes) on a bounded sample.
+          reads x, dy, writes dx) of the dominant launch over its CUDA-event
+          duration, against MEASURED_PEAKS.json hbm_gbs.
+--impl reference: the reference algorithm (the numpy oracle, pinned bit-exact to
+          the reference by tests/golden) on every host core, FULL workload,
+          channels split across processes; rank 0 only.
 """
 
 from __future__ import annotations
@@ -26,6 +34,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -103,38 +112,281 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_baseline(args, steps=3, warmup=1, sample_B=8):
-    """The oracle on every host core, bounded sample (subprocess: fork-safe)."""
-    cmd = [sys.executable, "-m", "oracle.cpu_bench", "--T", str(args.T), "--B", str(sample_B), "--C",
-           str(args.C), "--k", str(args.k), "--d", str(args.d), "--steps", str(steps), "--warmup", str(warmup)]
+# --------------------------------------------------------------------------
+# launch plumbing
+# --------------------------------------------------------------------------
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_if_needed(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: run N ranks under torch.distributed.run.
+    Returns the child's exit code, or None when this process is already a rank."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus and args.gpus != 1:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def batch_shard(B: int, rank: int, world: int, scaling: str) -> tuple[int, int]:
+    """(rows on this rank, global batch): strong scaling splits the global batch
+    B across the ranks (ddp.shard_bounds); weak scaling gives every rank B rows."""
+    from paper_2501_14490_b200 import ddp
+    if scaling == "weak":
+        return B, B * world
+    a, b = ddp.shard_bounds(B, rank, world)
+    return b - a, B
+
+
+# --------------------------------------------------------------------------
+# CPU legs (the oracle; only here and in --impl reference)
+# --------------------------------------------------------------------------
+def cpu_baseline(args, steps=2, warmup=1, one_core_channels=16):
+    """The oracle on every host core on the full workload + a 1-core figure
+    (subprocess: fork-safe, outside any timed region)."""
+    cmd = [sys.executable, "-m", "oracle.cpu_bench", "--T", str(args.T), "--B", str(args.B), "--C",
+           str(args.C), "--k", str(args.k), "--d", str(args.d), "--steps", str(steps), "--warmup", str(warmup),
+           "--one-core-channels", str(one_core_channels)]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, env={**os.environ, "OMP_NUM_THREADS": "1"})
     if r.returncode != 0:
         return {"value": None, "error": r.stderr.strip()[-400:]}
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+def _cpu_line(res):
+    one = res.get("one_core") or {}
+    return {"value": res.get("value"), "unit": UNIT, "cores": res.get("cores"), "kind": "port",
+            "sample": res.get("sample"), "cpu_model": res.get("cpu_model"), "host_cpus": res.get("host_cpus"),
+            "one_core": {"value": one.get("value"), "cores": 1, "sample": one.get("sample")} if one else None}
+
+
 def run_reference(args, rank: int, world: int):
-    """--impl reference: the reference algorithm on the host cores, rank 0 only."""
+    """--impl reference: the reference algorithm on the host cores, rank 0 only.
+    Each step is the full T*B*C workload (all channels, all batch rows), split
+    by channel across one process per core."""
     if rank != 0:
         return
-    # every step is one bounded sample (B=8 of the workload, ~40 ms on 16 cores),
-    # so the full --steps K --warmup W run stays within seconds to a minute
     steps, warmup = max(1, args.steps), max(0, args.warmup)
-    res = cpu_baseline(args, steps=steps, warmup=warmup)
+    res = cpu_baseline(args, steps=steps, warmup=warmup, one_core_channels=8)
     v = res.get("value")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": warmup, "ms_per_step": (res.get("seconds_per_step") or 0) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic N(0,1) x, dy; uniform(±k^-1/2) W",
         "config": {"workload": f"SpikingLayer TRAIN fwd+bwd T={args.T},B={args.B},C={args.C},k={args.k},"
-                               f"d={args.d} fp32 quantized (bounded sample B=8)",
-                   "parallelism": "host cores, channel split"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": res.get("cores"), "kind": "port",
-                         "sample": res.get("sample"), "cpu_model": res.get("cpu_model")},
+                               f"d={args.d} fp32 quantized (full workload every step)",
+                   "T": args.T, "B": args.B, "C": args.C, "k": args.k, "d": args.d,
+                   "parallelism": "host cores, channel split", "same_config": True},
+        "cpu_baseline": _cpu_line(res),
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if v is None:
+        line["error"] = res.get("error")
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+class Workload:
+    """One rank's share of the neuron layer step, driven through the C ABI:
+    spikes/dx and a GradBucket whose views receive dW, dgamma, dbeta."""
+
+    def __init__(self, P, L, dev, T, Bl, C, k, d, dt, seed, use_graph):
+        import numpy as np
+        import torch
+        from paper_2501_14490_b200 import ddp
+        self.torch, self.L = torch, L
+        self.nel = T * Bl * C
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.x = torch.randn((T, Bl, C), generator=g, device=dev).to(dt)
+        self.dy = torch.randn((T, Bl, C), generator=g, device=dev).to(dt)
+        cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+        self.layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(1), device=dev)
+        flags = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
+        self.desc = L.make_desc(self.x.shape, k, d, dt, flags=flags)
+        self.ws = L.workspace(self.desc, dev)
+        self.out = torch.empty_like(self.x)
+        self.dx = torch.empty_like(self.x)
+        self.fold = torch.empty((C, L.fold_stride(k)), dtype=torch.float64, device=dev)
+        lay = self.layer
+        self.bucket = ddp.GradBucket([lay.W, lay.gamma, lay.beta])
+        self.dW, self.dgam, self.dbet = self.bucket.views()
+        self.plan_f, self.plan_b = L.plan_info(self.desc, False), L.plan_info(self.desc, True)
+        self.stream = torch.cuda.current_stream(dev)
+        self.lib = L.lib()
+        if use_graph:
+            # one CUDA graph per direction and one for the whole step, captured
+            # from the same C-ABI calls (removes the per-call launch / ramp gap
+            # of the cooperative kernels, DESIGN.md section 5)
+            self.fwd(); self.bwd()
+            torch.cuda.synchronize()
+            gf, gb, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gf):
+                self.fwd(torch.cuda.current_stream().cuda_stream)
+            with torch.cuda.graph(gb):
+                self.bwd(torch.cuda.current_stream().cuda_stream)
+            with torch.cuda.graph(gs):
+                self.fwd(torch.cuda.current_stream().cuda_stream)
+                self.bwd(torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            self._graphs = (gf, gb, gs)
+            self.run_f, self.run_b, self.run_s = gf.replay, gb.replay, gs.replay
+        else:
+            self.run_f, self.run_b = self.fwd, self.bwd
+
+            def run_s():
+                self.fwd()
+                self.bwd()
+            self.run_s = run_s
+
+    def fwd(self, s=None):
+        lay, L = self.layer, self.L
+        L.check(self.lib.psn_forward_train(
+            ctypes.byref(self.desc), self.x.data_ptr(), lay.W.data_ptr(), lay.gamma.data_ptr(),
+            lay.beta.data_ptr(), lay.running_mean.data_ptr(), lay.running_var.data_ptr(), self.out.data_ptr(),
+            self.fold.data_ptr(), self.ws.data_ptr(), self.stream.cuda_stream if s is None else s))
+
+    def bwd(self, s=None):
+        lay, L = self.layer, self.L
+        L.check(self.lib.psn_backward(
+            ctypes.byref(self.desc), self.x.data_ptr(), self.dy.data_ptr(), lay.W.data_ptr(),
+            lay.gamma.data_ptr(), self.fold.data_ptr(), self.dx.data_ptr(), self.dW.data_ptr(),
+            self.dgam.data_ptr(), self.dbet.data_ptr(), self.ws.data_ptr(),
+            self.stream.cuda_stream if s is None else s))
+
+    def step(self, world):
+        self.run_s()
+        if world > 1:
+            self.bucket.reduce_()
+
+    def time_steps(self, K, warmup, world, dist):
+        torch = self.torch
+        for _ in range(warmup):
+            self.step(world)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(self.stream)
+        for _ in range(K):
+            self.step(world)
+        ev[1].record(self.stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / K
+
+    def time_directions(self, K):
+        torch = self.torch
+        evd = [torch.cuda.Event(enable_timing=True) for _ in range(3 * K)]
+        for i in range(K):
+            evd[3 * i].record(self.stream)
+            self.run_f()
+            evd[3 * i + 1].record(self.stream)
+            self.run_b()
+            evd[3 * i + 2].record(self.stream)
+        torch.cuda.synchronize()
+        f = [evd[3 * i].elapsed_time(evd[3 * i + 1]) for i in range(K)]
+        b = [evd[3 * i + 1].elapsed_time(evd[3 * i + 2]) for i in range(K)]
+        return statistics.mean(f), statistics.mean(b)
+
+
+def max_over_ranks(v, world, dist, dev):
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_e2e(P, wl, world, dist, K):
+    """The step through SpikingLayer autograd from pinned host memory: x, dy
+    H2D and spikes, dx, gradient bucket D2H every step.  Three streams (H2D,
+    compute, D2H) with two device slots, so step i's copies overlap step i+1's
+    input copy and step i-1's result copy, as a data loader would."""
+    import torch
+    lay, x, dy = wl.layer, wl.x, wl.dy
+    comp = wl.stream
+    s_in, s_out = torch.cuda.Stream(x.device), torch.cuda.Stream(x.device)
+    xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    dyh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    xh.copy_(x.cpu())
+    dyh.copy_(dy.cpu())
+    outh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for _ in range(2)]
+    dxh = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for _ in range(2)]
+    gh = [torch.empty(wl.bucket.flat.shape, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    xd = [torch.empty_like(x) for _ in range(2)]
+    dyd = [torch.empty_like(dy) for _ in range(2)]
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    comp_done = [torch.cuda.Event() for _ in range(2)]
+    d2h_done = [torch.cuda.Event() for _ in range(2)]
+    used = [False, False]
+
+    def one(i):
+        sl = i & 1
+        with torch.cuda.stream(s_in):
+            if used[sl]:
+                s_in.wait_event(comp_done[sl])  # the slot's previous step consumed its inputs
+            xd[sl].copy_(xh, non_blocking=True)
+            dyd[sl].copy_(dyh, non_blocking=True)
+            h2d_done[sl].record(s_in)
+        comp.wait_event(h2d_done[sl])
+        if used[sl]:
+            comp.wait_event(d2h_done[sl])  # host result buffers of this slot are free again
+        xi = xd[sl].requires_grad_(True)
+        for p in (lay.W, lay.gamma, lay.beta):
+            p.grad = None
+        out = lay(xi, P.Mode.TRAIN)
+        out.backward(dyd[sl])
+        wl.bucket.pack()
+        if world > 1:
+            wl.bucket.reduce_()
+        dx = xi.grad
+        xi.grad = None
+        xd[sl].requires_grad_(False)
+        comp_done[sl].record(comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(comp_done[sl])
+            out.record_stream(s_out)
+            dx.record_stream(s_out)
+            outh[sl].copy_(out, non_blocking=True)
+            dxh[sl].copy_(dx, non_blocking=True)
+            gh[sl].copy_(wl.bucket.flat, non_blocking=True)
+            d2h_done[sl].record(s_out)
+        used[sl] = True
+
+    for i in range(2):
+        one(i)
+    torch.cuda.synchronize()
+    ke = max(3, min(K, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    s_in.wait_stream(comp)
+    for i in range(ke):
+        one(i)
+    comp.wait_stream(s_in)
+    comp.wait_stream(s_out)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ems = max_over_ranks(e0.elapsed_time(e1) / ke, world, dist, x.device)
+    esize = x.element_size()
+    return {"ms_per_step": ems, "h2d_bytes_per_step": 2 * esize * wl.nel,
+            "d2h_bytes_per_step": 2 * esize * wl.nel + 8 * wl.bucket.flat.numel(),
+            "api": "paper_2501_14490_b200.SpikingLayer autograd; pinned host x/dy in, spikes/dx/grads out; "
+                   "H2D, compute and D2H on three streams (two device slots)"}
 
 
 def main():
@@ -143,6 +395,10 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: global batch --B split across ranks (default); weak: --B per rank")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: multi-rank tests on one device)")
     ap.add_argument("--T", type=int, default=1024)
     ap.add_argument("--B", type=int, default=64)
     ap.add_argument("--C", type=int, default=512)
@@ -151,9 +407,14 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-weak", action="store_true", help="N>1: skip the extra weak-scaling measurement")
     ap.add_argument("--no-graph", action="store_true", help="time direct C-ABI calls instead of CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        sys.exit(rc)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -163,125 +424,51 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2501_14490_b200 as P
     from paper_2501_14490_b200 import _lib as L
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local % max(ndev, 1))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
-    T, B, C, k, d = args.T, args.B, args.C, args.k, args.d
+    T, C, k, d = args.T, args.C, args.k, args.d
     dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     esize = 4 if dt == torch.float32 else 2
-    nel = T * B * C
-    lib = L.lib()
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    x = torch.randn((T, B, C), generator=g, device=dev).to(dt)
-    dy = torch.randn((T, B, C), generator=g, device=dev).to(dt)
-    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
-    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(1), device=dev)
-    flags = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
-    desc = L.make_desc(x.shape, k, d, dt, flags=flags)
-    ws = L.workspace(desc, dev)
-    out = torch.empty_like(x)
-    dx = torch.empty_like(x)
-    fold = torch.empty((C, L.PSN_FOLD_HDR + 2 * k), dtype=torch.float64, device=dev)
-    grads = torch.empty(C * k + 2 * C, dtype=torch.float64, device=dev)  # one flat DDP bucket
-    dW, dgam, dbet = grads[:C * k], grads[C * k:C * k + C], grads[C * k + C:]
-    stream = torch.cuda.current_stream(dev)
-    sp = stream.cuda_stream
-    W, gam, bet, rm, rv = layer.W.detach(), layer.gamma.detach(), layer.beta.detach(), layer.running_mean, layer.running_var
-
-    plan_f, plan_b = L.plan_info(desc, False), L.plan_info(desc, True)
-
-    def fwd(s=None):
-        L.check(lib.psn_forward_train(ctypes.byref(desc), x.data_ptr(), W.data_ptr(), gam.data_ptr(),
-                                      bet.data_ptr(), rm.data_ptr(), rv.data_ptr(), out.data_ptr(),
-                                      fold.data_ptr(), ws.data_ptr(), sp if s is None else s))
-
-    def bwd(s=None):
-        L.check(lib.psn_backward(ctypes.byref(desc), x.data_ptr(), dy.data_ptr(), W.data_ptr(), gam.data_ptr(),
-                                 fold.data_ptr(), dx.data_ptr(), dW.data_ptr(), dgam.data_ptr(), dbet.data_ptr(),
-                                 ws.data_ptr(), sp if s is None else s))
-
-    # The timed step replays one CUDA graph per direction (the workspace clear
-    # plus the persistent kernel), captured from the same C-ABI calls: this
-    # removes the per-call launch and ramp-up gap of the cooperative launch
-    # (~10 us fwd / ~5 us bwd when called directly).
-    # --no-graph times the direct calls instead.
-    if not args.no_graph:
-        fwd(); bwd()
-        torch.cuda.synchronize()
-        g_f, g_b, g_s = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_f):
-            fwd(torch.cuda.current_stream().cuda_stream)
-        with torch.cuda.graph(g_b):
-            bwd(torch.cuda.current_stream().cuda_stream)
-        with torch.cuda.graph(g_s):  # the whole step in one graph: no gap between the two launches
-            fwd(torch.cuda.current_stream().cuda_stream)
-            bwd(torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        run_f, run_b, run_s = g_f.replay, g_b.replay, g_s.replay
-    else:
-        run_f, run_b = fwd, bwd
-
-        def run_s():
-            fwd()
-            bwd()
-
-    def step():
-        run_s()
-        if world > 1:
-            dist.all_reduce(grads)
-
-    for _ in range(args.warmup):
-        step()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    Bl, Bg = batch_shard(args.B, rank, world, args.scaling)
+    wl = Workload(P, L, dev, T, Bl, C, k, d, dt, 1234 + rank, not args.no_graph)
     K = args.steps
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
-    with ClockSampler(local) as clk:
+
+    with ClockSampler(dev.index) as clk:
         t0 = time.perf_counter()
-        ev[0].record(stream)
-        for i in range(K):
-            run_s()
-            if world > 1:
-                dist.all_reduce(grads)
-            ev[i + 1].record(stream)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+        step_ms = wl.time_steps(K, args.warmup, world, dist)
         wall = time.perf_counter() - t0
-    step_ms = ev[0].elapsed_time(ev[K]) / K
-    # per-launch times for the roofline: the same K steps again, one direction per event pair
-    evd = [torch.cuda.Event(enable_timing=True) for _ in range(3 * K)]
-    for i in range(K):
-        evd[3 * i].record(stream)
-        run_f()
-        evd[3 * i + 1].record(stream)
-        run_b()
-        evd[3 * i + 2].record(stream)
-    torch.cuda.synchronize()
-    fwd_ms = [evd[3 * i].elapsed_time(evd[3 * i + 1]) for i in range(K)]
-    bwd_ms = [evd[3 * i + 1].elapsed_time(evd[3 * i + 2]) for i in range(K)]
-    t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms = float(t_local.item())
-    value = world * nel / (ms * 1e-3) / 1e9
+    ms = max_over_ranks(step_ms, world, dist, dev)
+    value = T * Bg * C / (ms * 1e-3) / 1e9
+    f_ms, b_ms = wl.time_directions(K)
+
+    weak = None
+    if world > 1 and not args.no_weak:
+        other = "weak" if args.scaling == "strong" else "strong"
+        Bl2, Bg2 = batch_shard(args.B, rank, world, other)
+        wl2 = Workload(P, L, dev, T, Bl2, C, k, d, dt, 4321 + rank, not args.no_graph)
+        ms2 = max_over_ranks(wl2.time_steps(K, args.warmup, world, dist), world, dist, dev)
+        weak = {"scaling": other, "value": T * Bg2 * C / (ms2 * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms2,
+                "B_per_gpu": Bl2, "global_batch": Bg2}
+        del wl2
 
     hbm, peak_src = _peaks()
-    f_ms, b_ms = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
+    nel = wl.nel
     fwd_bytes, bwd_bytes = 2 * esize * nel, 3 * esize * nel
-    fname = "psn_stream_kernel<fwd>" if plan_f.get("streamed") else "psn_forward_train (3 generic kernels)"
-    bname = "psn_stream_kernel<bwd>" if plan_b.get("streamed") else "psn_backward (3 generic kernels)"
+    fname = "psn_stream_kernel<fwd>" if wl.plan_f.get("streamed") else "psn_forward_train (3 generic kernels)"
+    bname = "psn_stream_kernel<bwd>" if wl.plan_b.get("streamed") else "psn_backward (3 generic kernels)"
     groups = {fname: (fwd_bytes, f_ms), bname: (bwd_bytes, b_ms)}
     dom_name, (dom_bytes, dom_ms) = max(groups.items(), key=lambda kv: kv[1][1])
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
@@ -290,73 +477,37 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         key = next((kk for kk in tr if (("1>" in kk) == ("bwd" in dom_name)) and f"<{k}, {d}, float" in kk), None)
-        if key is not None and args.dtype == "f32" and (T, B, C) == (1024, 64, 512):
+        if key is not None and args.dtype == "f32" and (T, Bl, C) == (1024, 64, 512):
             traffic = tr[key]["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         traffic = None
     step_achieved = (5 * esize * nel) / ((f_ms + b_ms) * 1e-3) / 1e9
 
-    # ---- e2e through the public module API with host buffers -----------------
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty((T, B, C), dtype=dt, pin_memory=True)
-        dyh = torch.empty((T, B, C), dtype=dt, pin_memory=True)
-        xh.copy_(x.cpu())
-        dyh.copy_(dy.cpu())
-        gh = torch.empty(C * k + 2 * C, dtype=torch.float64, pin_memory=True)
-        xd = torch.empty_like(x)
-        dyd = torch.empty_like(dy)
-
-        def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            dyd.copy_(dyh, non_blocking=True)
-            xi = xd.requires_grad_(True)
-            layer.zero_grad(set_to_none=True)
-            layer(xi, P.Mode.TRAIN).backward(dyd)
-            flat = torch.cat([layer.W.grad.flatten(), layer.gamma.grad, layer.beta.grad])
-            if world > 1:
-                dist.all_reduce(flat)
-            gh.copy_(flat, non_blocking=True)
-            xd.requires_grad_(False)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        ke = max(3, min(K, 10))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(ke):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / ke
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        ems = float(te.item())
-        e2e = {"value": world * nel / (ems * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": 2 * esize * nel, "d2h_bytes_per_step": 8 * (C * k + 2 * C),
-               "api": "paper_2501_14490_b200.SpikingLayer autograd, pinned host x/dy"}
+        e = run_e2e(P, wl, world, dist, K)
+        e2e = {"value": T * Bg * C / (e["ms_per_step"] * 1e-3) / 1e9, "unit": UNIT, **e}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args)
-        if cpu.get("value") is not None:
-            cpu = {"value": cpu["value"], "unit": UNIT, "cores": cpu["cores"], "kind": "port",
-                   "sample": cpu["sample"], "cpu_model": cpu.get("cpu_model")}
+        res = cpu_baseline(args)
+        cpu = _cpu_line(res) if res.get("value") is not None else res
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic N(0,1) x and dy, uniform(±k^-1/2) W, gamma=1, beta=-1",
             "config": {"workload": f"SpikingLayer TRAIN fwd+bwd, quantized, batch-stat BN fusion, "
-                                   f"T={T},B={B},C={C},k={k},d={d}, {args.dtype} I/O (BASELINE configs[4] "
-                                   f"at the metric shape)",
-                       "T": T, "B_per_gpu": B, "C": C, "k": k, "d": d, "parallelism": f"dp{world}",
+                                   f"T={T},B={Bg},C={C},k={k},d={d}, {args.dtype} I/O (BASELINE metric shape; "
+                                   f"{args.scaling} scaling, B={Bl} on rank 0)",
+                       "T": T, "global_batch": Bg, "B_per_gpu": Bl, "C": C, "k": k, "d": d,
+                       "parallelism": f"dp{world}",
                        "launch": "direct C-ABI calls" if args.no_graph else
-                                 "CUDA-graph replay of the C-ABI calls (one graph per direction)",
-                       "l2": "inputs larger than L2 (x, dy each %.0f MB > 126 MB L2)" % (nel * esize / 1e6)},
+                                 "CUDA-graph replay of the C-ABI calls (fwd+bwd in one graph)",
+                       "l2": "inputs larger than L2 (x, dy each %.0f MB vs 126 MB L2)" % (nel * esize / 1e6)
+                             if nel * esize > 126e6 else
+                             "per-rank inputs (%.0f MB) fit L2; consecutive steps reuse them" % (nel * esize / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": dom_name,
                          "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
@@ -365,11 +516,13 @@ def main():
                               "bytes_per_step": 5 * esize * nel, "fwd_ms": f_ms, "bwd_ms": b_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * (plan_f["launches"] + plan_b["launches"]),
-            "plan": {"forward": plan_f, "backward": plan_b},
+            "gpu_launches": K * (wl.plan_f["launches"] + wl.plan_b["launches"]),
+            "plan": {"forward": wl.plan_f, "backward": wl.plan_b},
             "clocks": clk.summary(),
             "wall_s_timed": wall,
         }
+        if weak is not None:
+            line["weak"] = weak
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -45,7 +45,7 @@ extern "C" {
 /* == cudaStream_t; declared opaquely so this header needs no CUDA headers */
 typedef struct CUstream_st *psn_stream_t;
 
-#define PSN_ABI_VERSION 1
+#define PSN_ABI_VERSION 2
 #define PSN_MAX_ORDER 16
 
 typedef enum {
@@ -85,9 +85,14 @@ typedef struct {
 
 /* Per-channel forward state ("fold") the backward consumes; float64,
  * psn_fold_doubles(desc) values = C * PSN_FOLD_STRIDE(k), row c:
- *   [mu*, s, a, b_f, mu_batch, var_batch, w_f[0..k), w_q[0..k)]                */
-#define PSN_FOLD_HDR 6
-#define PSN_FOLD_STRIDE(k) (PSN_FOLD_HDR + 2 * (k))
+ *   [mu*, s, a, b_f, mu_batch, var_batch, bn_sums, w_f[0..k), w_q[0..k),
+ *    Sx[0..k), Cx[0..k)]
+ * Sx[i] = sum_(t,n,q) x[t-off_i] and Cx[i] = sum x[t-off_i] (h1[t] - mu_batch)
+ * are the data terms of the BN-through-statistics weight gradient
+ * (network.py:298-315); the streamed forward writes them (bn_sums = 1) and the
+ * streamed backward requires them (it traps if bn_sums != 1).                  */
+#define PSN_FOLD_HDR 7
+#define PSN_FOLD_STRIDE(k) (PSN_FOLD_HDR + 4 * (k))
 
 PSN_API const char *psn_last_error(void);          /* thread-local message of last failure */
 PSN_API int psn_abi_version(void);

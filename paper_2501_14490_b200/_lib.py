@@ -26,7 +26,12 @@ PSN_USE_BATCH_STATS = 4
 PSN_SMOOTH = 8
 PSN_QUANTIZE_IN_SMOOTH = 16
 PSN_ROUND_STE = 32
-PSN_FOLD_HDR = 6
+PSN_FOLD_HDR = 7
+
+
+def fold_stride(k: int) -> int:
+    """Doubles per channel of the forward's fold state (PSN_FOLD_STRIDE)."""
+    return PSN_FOLD_HDR + 4 * int(k)
 
 EXPORTED = (
     "psn_last_error", "psn_abi_version", "psn_max_order", "psn_fold_doubles",
@@ -132,6 +137,16 @@ def make_desc(shape, k: int, d: int, dtype: torch.dtype, flags: int = 0,
 
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
+
+
+def run(t: torch.Tensor, name: str, *args) -> None:
+    """Call C-ABI entry point `name` with t's device current (so the launch, the
+    stream handle from stream_of(t) and the per-device plan attributes all refer
+    to the device that owns the pointers) and raise on a non-OK status."""
+    fn = getattr(lib(), name)
+    with torch.cuda.device(t.device):
+        rc = fn(*args)
+    check(rc)
 
 
 def stream_of(t: torch.Tensor) -> int:

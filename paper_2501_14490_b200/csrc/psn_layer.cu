@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kThreads) fwd_fold_kernel(Geom g, const double
   f[3] = b_f;
   f[4] = mu_b;
   f[5] = var_b;
+  f[6] = 0.0;  // no BN-term data sums (the generic backward forms its own)
   for (int i = 0; i < K; ++i) {
     const double wf = a * Wc[i];
     f[PSN_FOLD_HDR + i] = wf;
@@ -798,10 +799,10 @@ int psn_forward_train(const psn_desc_t* desc, const void* x, const double* W, co
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
   stream::Plan P;
-  if (stream::make_plan(desc, false, P)) {
+  if (stream::aligned_for_tma(x, out) && stream::make_plan(desc, false, P)) {
     rc = stream::forward(desc, P, x, W, gamma, beta, running_mean, running_var, out, fold,
                          (char*)workspace + L.fused, (cudaStream_t)stream);
-    return rc ? rc : cuda_check("psn_forward_train (stream)");
+    if (rc != stream::kFallback) return rc ? rc : cuda_check("psn_forward_train (stream)");
   }
   return by_dtype_k<FwdOp>(desc, desc, g, x, W, gamma, beta, running_mean, running_var, out, fold,
                            (char*)workspace, L, (cudaStream_t)stream);
@@ -821,14 +822,16 @@ int psn_backward(const psn_desc_t* desc, const void* x, const void* dy, const do
   const Geom g = plan(desc);
   const WsLayout L = ws_layout(desc);
   stream::Plan P;
-  if (stream::make_plan(desc, true, P)) {
+  if (stream::aligned_for_tma(x, dy) && stream::make_plan(desc, true, P)) {
     double* dwtmp = (double*)((char*)workspace + L.dwtmp);
     const bool shared = desc->flags & PSN_SHARED;
     rc = stream::backward(desc, P, x, dy, W, gamma, fold, dx, shared ? dwtmp : dW, dgamma, dbeta,
                           (char*)workspace + L.fused, (cudaStream_t)stream);
-    if (rc) return rc;
-    if (shared) shared_rowsum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dwtmp, desc->C, desc->k, dW);
-    return cuda_check("psn_backward (stream)");
+    if (rc != stream::kFallback) {
+      if (rc) return rc;
+      if (shared) shared_rowsum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dwtmp, desc->C, desc->k, dW);
+      return cuda_check("psn_backward (stream)");
+    }
   }
   return by_dtype_k<BwdOp>(desc, desc, g, x, dy, W, gamma, fold, dx, dW, dgamma, dbeta, (char*)workspace, L,
                            (cudaStream_t)stream);

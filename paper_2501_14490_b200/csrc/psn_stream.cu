@@ -13,15 +13,19 @@
 namespace psn {
 namespace stream {
 
-static int g_sms = 0, g_smem_optin = 0;
-static std::once_flag g_dev_once;
+// Device attributes are looked up per device (the current device of the
+// calling thread, which the caller sets to the device of its pointers), once
+// per device.
+constexpr int kMaxDevices = 64;
+struct DevAttr {
+  int sms = 0, smem_optin = 0, coop = 0;
+};
+static DevAttr g_dev[kMaxDevices];
+static std::once_flag g_dev_once[kMaxDevices];
+static std::once_flag g_encode_once;
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-static void dev_init() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+static void encode_init() {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
@@ -30,9 +34,38 @@ static void dev_init() {
   cudaGetLastError();
 }
 
+static const DevAttr* dev_attr() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::call_once(g_dev_once[dev], [dev] {
+    DevAttr& a = g_dev[dev];
+    cudaDeviceGetAttribute(&a.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&a.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&a.coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaGetLastError();
+  });
+  std::call_once(g_encode_once, encode_init);
+  return &g_dev[dev];
+}
+
+bool aligned_for_tma(const void* x, const void* dy) {
+  return (((uintptr_t)x | (uintptr_t)dy) & 15u) == 0;  // TMA global addresses are 16-byte aligned
+}
+
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
+}
+
+// watchdog of the in-kernel waits: PSN_WAIT_LIMIT_MS (default 4000 ms; 0 turns
+// it off, e.g. under compute-sanitizer or a debugger)
+static unsigned long long wait_limit_ns() {
+  const char* e = getenv("PSN_WAIT_LIMIT_MS");
+  const long long ms = e ? atoll(e) : 4000;
+  return ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
 }
 
 bool eligible(const psn_desc_t* desc) {
@@ -50,8 +83,9 @@ bool eligible(const psn_desc_t* desc) {
 
 bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   if (!eligible(desc)) return false;
-  std::call_once(g_dev_once, dev_init);
-  if (!g_encode || g_sms <= 0) return false;
+  const DevAttr* da = dev_attr();
+  if (!da || !g_encode || da->sms <= 0 || !da->coop) return false;
+  const int g_sms = da->sms, g_smem_optin = da->smem_optin;
   const int es = (int)dtype_size(desc->dtype);
   if (desc->T > (1 << 24) || desc->C > (1 << 24)) return false;  // group / iteration indices stay small
   if ((double)desc->T * desc->N * desc->C >= 4294967296.0) return false;  // 32-bit element offsets
@@ -103,11 +137,14 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-// workspace: group counters (pass 1, pass 2) | per-channel f64 sums of pass 1 |
-// forward pass-2 sums -- all zeroed per launch
+// workspace, all zeroed per launch: group counters cnt[G], cntA[G] | exponent
+// keys emax[G][NV][32] (u32) | per-channel sums acc[G][NV][32] (f64)
+static size_t counter_bytes(const Plan& p) { return a256(2 * sizeof(unsigned) * p.G); }
+static size_t emax_bytes(const Plan& p, bool bwd) {
+  return a256(sizeof(unsigned) * (size_t)p.G * layout_of(p.k, p.d, 4, bwd).NV * kCols);
+}
 static size_t zeroed_bytes(const Plan& p, bool bwd) {
-  const Layout L = layout_of(p.k, p.d, 4, bwd);
-  return a256(2 * sizeof(unsigned) * p.G) + sizeof(double) * p.G * (L.NV + L.NV2) * kCols;
+  return counter_bytes(p) + emax_bytes(p, bwd) + sizeof(double) * (size_t)p.G * layout_of(p.k, p.d, 4, bwd).NV * kCols;
 }
 
 size_t workspace_bytes(const psn_desc_t* desc) {
@@ -143,18 +180,17 @@ int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const voi
 
 struct Ws {
   unsigned* cnt;
-  unsigned* cnt2;
+  unsigned* cntA;
+  unsigned* emax;
   double* acc;
-  double* acc2;
 };
 
 static Ws carve(void* ws, const Plan& p, bool bwd) {
-  const Layout L = layout_of(p.k, p.d, 4, bwd);
   Ws w;
   w.cnt = (unsigned*)ws;
-  w.cnt2 = w.cnt + p.G;
-  w.acc = (double*)((char*)ws + a256(2 * sizeof(unsigned) * p.G));
-  w.acc2 = w.acc + (size_t)p.G * L.NV * kCols;
+  w.cntA = w.cnt + p.G;
+  w.emax = (unsigned*)((char*)ws + counter_bytes(p));
+  w.acc = (double*)((char*)ws + counter_bytes(p) + emax_bytes(p, bwd));
   return w;
 }
 
@@ -181,13 +217,15 @@ int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* 
   a.rv = rv;
   a.fold = fold;
   a.cnt = w.cnt;
+  a.cntA = w.cntA;
+  a.emax = w.emax;
   a.acc = w.acc;
-  a.cnt2 = w.cnt2;
-  a.acc2 = w.acc2;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;
   a.momentum = desc->momentum;
+  a.x = x;
+  a.wait_ns = wait_limit_ns();
   a.trace = env_int("PSN_TRACE", 0);
   a.ablate = env_int("PSN_ABLATE", 0);
   return dispatch(desc, false, a, x, nullptr, st);
@@ -210,13 +248,15 @@ int backward(const psn_desc_t* desc, const Plan& p, const void* x, const void* d
   a.dgamma = dgamma;
   a.dbeta = dbeta;
   a.cnt = w.cnt;
+  a.cntA = w.cntA;
+  a.emax = w.emax;
   a.acc = w.acc;
-  a.cnt2 = w.cnt2;
-  a.acc2 = w.acc2;
   a.flags = desc->flags;
   a.shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   a.eps = desc->eps;
   a.momentum = desc->momentum;
+  a.x = x;
+  a.wait_ns = wait_limit_ns();
   a.trace = env_int("PSN_TRACE", 0);
   a.ablate = env_int("PSN_ABLATE", 0);
   Surrogate s;

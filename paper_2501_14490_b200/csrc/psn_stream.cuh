@@ -33,9 +33,10 @@
 // time-reversed conv needs.
 //
 // Work is assigned statically (contiguous tile ranges per CTA, rotated per
-// group so remainders spread) and every CTA reduces its sums in a fixed order;
-// the cross-CTA f64 atomic adds make results reproducible to ~1 ulp of those
-// sums.
+// group so remainders spread).  Every CTA reduces its sums in a fixed order;
+// across CTAs the partials are added EXACTLY (publish_exact), so the totals do
+// not depend on the order the CTAs arrive in: results are bitwise reproducible
+// run to run (the reference is, tests/test_train.py:70-82).
 #pragma once
 
 #include <cuda.h>
@@ -84,9 +85,6 @@ constexpr int kRowBlock = 4;                     // time rows a consumer thread 
 #define PSN_TRACE_BUILD 0  // 1: per-CTA wait/compute breakdown (PSN_TRACE=1 at run time)
 #endif
 
-#ifndef PSN_WAIT_LIMIT_NS
-#define PSN_WAIT_LIMIT_NS 4000000000ull
-#endif
 
 // -------------------------------------------------------------------------
 // plan + arguments (plain data, passed by value)
@@ -118,10 +116,12 @@ struct Args {
   double* dW;             // [C,k] (or per-channel scratch when shared)
   double* dgamma;
   double* dbeta;
-  double* acc;            // [G][NV][32] per-channel pass-1 sums (f64 atomic adds, zeroed per launch)
+  double* acc;            // [G][NV][32] per-channel pass-1 sums (exact adds, publish_exact)
+  unsigned* emax;         // [G][NV][32] largest biased exponent of the CTA partials, + 1 (0: none)
   unsigned* cnt;          // [G] pass-1 arrivals (every CTA arrives once per group)
-  double* acc2;           // [G][k][32] backward pass-2 BN-term sums (f64 atomic adds, zeroed)
-  unsigned* cnt2;         // [G] backward pass-2 arrivals
+  unsigned* cntA;         // [G] exponent-agreement arrivals (all four zeroed per launch)
+  const void* x;          // the input (forward: one sample per channel sets the moment shift)
+  unsigned long long wait_ns;  // watchdog of every wait (0: off); PSN_WAIT_LIMIT_MS at run time
   int flags;
   int shared;
   double eps, momentum;
@@ -182,12 +182,13 @@ __device__ __forceinline__ bool mbar_try_hint(uint64_t* b, unsigned parity, unsi
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+// `lim` (ns, 0 = no watchdog) turns a hang into a trap with a message
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, unsigned long long lim) {
   if (mbar_try(b, parity)) return;
   const unsigned long long t0 = gtimer();
   for (unsigned n = 1;; ++n) {
     if (mbar_try_hint(b, parity, 20000u)) return;
-    if ((n & 63u) == 0 && gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired("mbarrier", (int)parity, 0);
+    if ((n & 63u) == 0 && lim && gtimer() - t0 > lim) expired("mbarrier", (int)parity, 0);
   }
 }
 
@@ -228,13 +229,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
 }
 // one thread waits for a grid counter (co-residency is guaranteed by the
 // cooperative launch); callers publish the result with a CTA barrier
-__device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target, const char* what) {
+__device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target, const char* what,
+                                             unsigned long long lim) {
   if (ld_acquire(a) >= target) return;
   const unsigned long long t0 = gtimer();
   unsigned v;
   while ((v = ld_acquire(a)) < target) {
     __nanosleep(1000);
-    if (gtimer() - t0 > PSN_WAIT_LIMIT_NS) expired(what, (int)v, (int)target);
+    if (lim && gtimer() - t0 > lim) expired(what, (int)v, (int)target);
   }
 }
 
@@ -300,19 +302,19 @@ __host__ __device__ constexpr int tile_rows(int es, bool bwd) { return bwd ? (es
 __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   Layout L{};
   L.H = (k - 1) * d;
-  L.NV = bwd ? 1 + k : 2;   // pass-1 sums: fwd S1, S2; bwd db, dw_q[k]
-  L.NV2 = bwd ? k : 0;  // backward pass-2 BN-term sums sum_t x[t-off_i] dh1[t]
+  L.NV = bwd ? 1 + k : 2 + 2 * k;  // pass-1 sums: fwd S1, S2, P[k], Sx[k]; bwd db, dw_q[k]
+  L.NV2 = 0;
   L.TB = tile_rows(es, bwd);
   L.rowb = kBoxN * kCols * es;  // bytes of one time row of a box
   const int xrows = L.TB > L.H ? L.TB : L.H;
   L.xbytes = xrows * L.rowb;
   L.dbytes = bwd ? xrows * L.rowb : 0;
-  // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
-  // per-lane pass-2 parameters: fwd f64 w_q[k], b_f; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1
-  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 3) + 15) / 16 * 16 : 8 * (k + 1);
+  // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1, c
+  // per-lane pass-2 parameters: fwd f64 w_q[k], b_f; bwd f64 w_q[k], b_f' + f32 W[k], mu', a1, b1, c
+  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 4) + 15) / 16 * 16 : 8 * (k + 1);
   L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
   L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
-  L.dep = 8 * (L.NV > L.NV2 ? L.NV : L.NV2) * kCols * 8;  // per-warp-pair partial sums handed to the publisher
+  L.dep = 8 * L.NV * kCols * 8;  // per-warp-pair partial sums handed to the publisher
   L.tot = 8 * 2 * kCols * 8;                  // publisher ring: pre-update running stats of 8 groups
   L.fixed = L.dep + 4 * L.pbytes + L.tot + 512;
   return L;
@@ -357,15 +359,17 @@ __device__ __forceinline__ Team team_of(const Plan& p) {
 }
 // worker index of this CTA for local group j (rotated per group and pass, so
 // the idle members and the short ranges move around the team)
-__device__ __forceinline__ int worker_of(const Team& t, int j, int pass) {
+__device__ __forceinline__ int worker_of_member(const Team& t, int mm, int j, int pass) {
   const unsigned n = (unsigned)t.sz;
   const unsigned rot = ((unsigned)j * 61u + (unsigned)pass * 29u) % n;
-  return (int)(((unsigned)t.m + n - rot) % n);
+  return (int)(((unsigned)mm + n - rot) % n);
 }
+__device__ __forceinline__ int worker_of(const Team& t, int j, int pass) { return worker_of_member(t, t.m, j, pass); }
 __device__ __forceinline__ void tile_range(const Plan& p, const Team& t, int v, int& ta, int& tb) {
   ta = (int)((unsigned)v * (unsigned)p.tpg / (unsigned)t.P);
   tb = (int)((unsigned)(v + 1) * (unsigned)p.tpg / (unsigned)t.P);
 }
+
 
 enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
 
@@ -382,6 +386,7 @@ template <int K, bool BWD>
 struct FoldIn {
   double W[K], gamma, beta;
   double mu, s, aa, bf, wf[BWD ? K : 1], wq[BWD ? K : 1];  // the forward's fold row (backward only)
+  double sx[BWD ? K : 1], cx[BWD ? K : 1], bn;               // ... and its BN-term data sums
 };
 template <int K, bool BWD>
 __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD>& in) {
@@ -397,10 +402,13 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
     in.s = __ldg(fr + 1);
     in.aa = __ldg(fr + 2);
     in.bf = __ldg(fr + 3);
+    in.bn = __ldg(fr + 6);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       in.wf[i] = __ldg(fr + PSN_FOLD_HDR + i);
       in.wq[i] = __ldg(fr + PSN_FOLD_HDR + K + i);
+      in.sx[i] = __ldg(fr + PSN_FOLD_HDR + 2 * K + i);
+      in.cx[i] = __ldg(fr + PSN_FOLD_HDR + 3 * K + i);
     }
   }
 }
@@ -414,8 +422,8 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
 // -------------------------------------------------------------------------
 template <int K, bool BWD>
 __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<K, BWD>& in, const double* tt,
-                                             double rm_prev, double rv_prev, bool store, unsigned char* prow,
-                                             const double* sxs = nullptr) {
+                                             double rm_prev, double rv_prev, double sh, bool store,
+                                             unsigned char* prow) {
   const Plan& p = a.p;
   double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
   double* pd = (double*)prow;
@@ -426,7 +434,7 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
     const bool use_batch = flags & PSN_USE_BATCH_STATS;
     const bool quantize = (flags & PSN_QUANTIZED) && (!smooth || (flags & PSN_QUANTIZE_IN_SMOOTH));
     const double dmean = tt[0] / m;
-    const double mu_b = rm_prev + dmean;  // the pass-1 shift was running_mean (pre-update)
+    const double mu_b = sh + dmean;  // pass-1 moments are shifted by one h1 sample of the channel
     double var_b = tt[1] / m - dmean * dmean;
     var_b = var_b < 0.0 ? 0.0 : var_b;
     const double mu = use_batch ? mu_b : rm_prev;  // network.py:250-255
@@ -450,6 +458,16 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       fr[3] = bf;
       fr[4] = mu_b;
       fr[5] = var_b;
+      fr[6] = 1.0;  // BN-term data sums present
+      // data terms of the BN-through-statistics dW (network.py:298-315), exact in
+      // f64: Sx_i = sum x[t-off_i], Cx_i = sum x[t-off_i] (h1[t] - mu_b); pass 1
+      // summed P_i = sum x[t-off_i] (h1[t] - shift)
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const double sx = tt[2 + K + i];
+        fr[PSN_FOLD_HDR + 2 * K + i] = sx;
+        fr[PSN_FOLD_HDR + 3 * K + i] = tt[2 + i] - (mu_b - sh) * sx;
+      }
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -492,24 +510,38 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       alpha1 = dmu / m;
       beta1 = (2.0 / m) * dvar;
     }
-    if (sxs != nullptr) {  // kernel tail: dW plus the BN term sum_t x[t-off_i] dh1[t] of pass 2
-#pragma unroll
-      for (int i = 0; i < K; ++i) a.dW[(size_t)c * K + i] = aa * dwf[i] + sxs[i];  // network.py:298-315
-      return;
-    }
     if (store) {
       a.dbeta[c] = db_f;
       a.dgamma[c] = da / s;
+      // dW = a dw_f + sum_t x[t-off_i] dh1[t] with dh1 = alpha1 + beta1 (h1 - mu):
+      // the BN term from the forward's exact data sums (network.py:298-315)
+      const bool bnt = flags & PSN_USE_BATCH_STATS;
+      if (bnt && in.bn != 1.0) {
+        printf("psn stream backward: the fold has no BN-term sums (forward not run by the streamed kernel)\n");
+        __trap();
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        a.dW[(size_t)c * K + i] = aa * dwf[i] + (bnt ? alpha1 * in.sx[i] + beta1 * in.cx[i] : 0.0);
     }
+    // pass 2 runs in f32 on centred inputs x - c (c: the channel's mean input,
+    // from the forward's data sums): h1 - mu and h2 then carry no large common
+    // offset the f32 arithmetic would have to cancel (inputs like x + 50);
+    // masked taps hold -c so that x = 0 there, as the reference skips them
+    const double cx = in.bn == 1.0 ? (double)(float)(in.sx[K - 1] / m) : 0.0;
+    double sw = 0.0, swq = 0.0;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       pd[i] = in.wq[i];
       pf[i] = (float)in.W[i];
+      sw += in.W[i];
+      swq += in.wq[i];
     }
-    pd[K] = in.bf;
-    pf[K] = (float)mu;
+    pd[K] = in.bf + cx * swq;
+    pf[K] = (float)(mu - cx * sw);
     pf[K + 1] = (float)alpha1;
     pf[K + 2] = (float)beta1;
+    pf[K + 3] = (float)cx;
   }
 }
 
@@ -518,8 +550,50 @@ __device__ __forceinline__ bool designated(const Team& t, int j) {
   return (int)(((unsigned)j * 37u + 11u) % (unsigned)t.sz) == t.m;
 }
 
+// Exact, order-independent sum of one value over the team's CTAs (phase B of
+// the publisher): every partial is rounded to the grid 2^q with
+// q = E + ceil(log2 P) - 53, where 2^E bounds the largest |partial| of the
+// value (agreed in phase A by an integer atomicMax on the exponents).  All
+// partials and all their partial sums are then integer multiples of 2^q below
+// 2^(q+53), so every f64 addition is exact and the total is the same whatever
+// order the atomic adds land in.  The rounding moves a partial by at most
+// 2^(q-1) = 2^-54 * P * 2^E (relative 1e-15 of the largest partial).
+__device__ __forceinline__ unsigned exp_key(double v) {  // biased exponent + 1 (>= 2 for v != 0)
+  const unsigned be = (unsigned)((__double_as_longlong(v) >> 52) & 0x7FF);
+  return (be > 1u ? be : 1u) + 1u;
+}
+__device__ __forceinline__ double round_to_agreed_grid(double v, unsigned key, int lgP) {
+  const int E = (int)key - 1 - 1022;  // |partial| < 2^E for every partial of the value
+  int q = E + lgP - 53;
+  q = q < -1074 ? -1074 : q;
+  return ldexp(rint(ldexp(v, -q)), q);
+}
 __device__ __forceinline__ void red_add_f64(double* a, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ float ld_io(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ld_io(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+
+// Shift of the forward's pass-1 moments for column c: h1 of stream (n = 0, c)
+// at t = T - 1, computed like the consumers compute h1.  One sample of the
+// channel's own distribution lies within a few standard deviations of its
+// mean, so the one-pass moments sum (h1 - shift) without the cancellation a
+// far-away shift (e.g. a stale running mean) would cause.  Every CTA derives
+// the same value from the same data.
+template <int K, int D, typename IO>
+__device__ __forceinline__ double group_shift(const Args& a, const double* w, int c) {
+  const Plan& p = a.p;
+  const IO* x = (const IO*)a.x;
+  const int ts = p.T - 1;
+  double h = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int t = ts - (K - 1 - i) * D;
+    const double xv = t >= 0 ? (double)ld_io(x + ((size_t)t * p.N) * p.J + c) : 0.0;
+    h = i == 0 ? w[0] * xv : fma(w[i], xv, h);
+  }
+  return round_f32_sg(h);
 }
 
 // -------------------------------------------------------------------------
@@ -586,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue = [&](int kind, int pass, int g, int nbi, int trow) {
         if (q >= p.S) {
           const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-          mbar_wait(empty + s, ph ^ 1u);
+          mbar_wait(empty + s, ph ^ 1u, a.wait_ns);
           if (PSN_TRACE_BUILD && a.trace) tr_empty += gtimer() - t0;
         }
         unsigned char* st = smem + (size_t)s * C_::STAGE;
@@ -667,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // consumers' done_p1(j - 2))
     auto stage_p1 = [&](int j) {
       if (j >= 2) {
-        if (lane == 0) mbar_wait(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1));
+        if (lane == 0) mbar_wait(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
         __syncwarp();
       }
       const int c = gid(j) * kCols + lane;
@@ -676,9 +750,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       double* d = (double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
       if constexpr (!BWD) {
         const double* Wc = a.W + (size_t)(a.shared ? 0 : cc) * K;
+        double wl[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) d[i] = cv ? __ldg(Wc + i) : 0.0;
-        d[K] = cv ? __ldcg(a.rm + cc) : 0.0;  // shift of the pass-1 moments (pre-update running mean)
+        for (int i = 0; i < K; ++i) {
+          wl[i] = cv ? __ldg(Wc + i) : 0.0;
+          d[i] = wl[i];
+        }
+        d[K] = cv ? group_shift<K, D, IO>(a, wl, cc) : 0.0;  // shift of the pass-1 moments
       } else {
         const double* f = a.fold + (size_t)cc * PSN_FOLD_STRIDE(K);
 #pragma unroll
@@ -691,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tm.ng > 0) stage_p1(0);
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
       const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1));
+      if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1), a.wait_ns);
       __syncwarp();
       if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
 #pragma unroll
@@ -709,9 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (int it = 0; it < iters; ++it) {
       const bool p1 = it < tm.ng;
-      const int j2 = it - p.lag;
-      const bool p2 = BWD && j2 >= 0 && j2 < tm.ng;  // backward pass-2 BN-term sums of local group it - lag
-      const int g1 = gid(it), g2 = gid(j2);
+      const int g1 = gid(it);
       if (it + 1 < tm.ng) stage_p1(it + 1);
       if (p1) {
         if (!BWD) {
@@ -719,28 +795,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
           if (it + 1 < tm.ng) prefetch_stats(gid(it + 1));
         }
-        if (worker_of(tm, it, 0) < tm.P) {
-          double t[kMaxNV];
+        const bool wk = worker_of(tm, it, 0) < tm.P;
+        double t[kMaxNV];
+        unsigned* em = a.emax + (size_t)g1 * NV * kCols + lane;
+        // phase A: agree on the largest exponent of each value's partials
+        if (wk) {
           take_deposit(NV, t);
 #pragma unroll
-          for (int val = 0; val < NV; ++val) red_add_f64(a.acc + ((size_t)g1 * NV + val) * kCols + lane, t[val]);
+          for (int val = 0; val < NV; ++val)
+            if (t[val] != 0.0) atomicMax(em + val * kCols, exp_key(t[val]));
         }
-      }
-      if constexpr (BWD) {
-        if (p2 && worker_of(tm, j2, 1) < tm.P && !(a.ablate & 16)) {
-          double t[kMaxNV];
-          take_deposit(LY.NV2, t);
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cntA + g1) : "memory");
+        }
+        // phase B: exact adds on the agreed grid (every member arrived in phase A)
+        if (wk) {
+          if (lane == 0) wait_counter(a.cntA + g1, (unsigned)tm.sz, "exponent agreement", a.wait_ns);
+          __syncwarp();
+          const int lgP = tm.P > 1 ? 32 - __clz(tm.P - 1) : 0;
 #pragma unroll
-          for (int val = 0; val < LY.NV2; ++val)
-            red_add_f64(a.acc2 + ((size_t)g2 * LY.NV2 + val) * kCols + lane, t[val]);
+          for (int val = 0; val < NV; ++val) {
+            const unsigned key = __ldcg(em + val * kCols);
+            if (t[val] != 0.0)
+              red_add_f64(a.acc + ((size_t)g1 * NV + val) * kCols + lane, round_to_agreed_grid(t[val], key, lgP));
+          }
         }
-      }
-      // one release fence for this iteration's atomics, then relaxed arrivals
-      __syncwarp();
-      if (lane == 0 && (p1 || p2)) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (p1) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + g1) : "memory");
-        if (p2) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt2 + g2) : "memory");
+        // one release fence for this group's adds, then a relaxed arrival
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + g1) : "memory");
+        }
       }
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
@@ -762,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       FoldIn<K, BWD> in;
       if (c < p.C) load_fold_in<K, BWD>(a, c, in);
       unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)tm.sz, "pass-1 sums");
+      if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)tm.sz, "pass-1 sums", a.wait_ns);
       __syncwarp();
       if (PSN_TRACE_BUILD && a.trace) {
         const unsigned long long t1 = gtimer();
@@ -770,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         t0 = t1;
       }
       if (j >= 2) {
-        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((j >> 1) - 1) & 1));
+        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
         __syncwarp();
       }
       if (c < p.C) {
@@ -779,7 +866,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
         const double rmp = BWD ? 0.0 : prev[((j & 7) * 2 + 0) * kCols + lane];
         const double rvp = BWD ? 0.0 : prev[((j & 7) * 2 + 1) * kCols + lane];
-        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, designated(tm, j),
+        double sh = 0.0;
+        if constexpr (!BWD) sh = group_shift<K, D, IO>(a, in.W, c);
+        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, sh, designated(tm, j),
                              p2s + sl * LY.pbytes + lane * LY.pstride);
       } else {
         double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
@@ -789,25 +878,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p2f + sl);
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
-    }
-    if constexpr (BWD) {  // dW once every CTA streamed the group's pass 2 (BN-term sums)
-      for (int j = 0; j < tm.ng; ++j) {
-        if (!designated(tm, j)) continue;
-        const int g = gid(j);
-        const int c = g * kCols + lane;
-        FoldIn<K, BWD> in;
-        if (c < p.C) load_fold_in<K, BWD>(a, c, in);
-        if (lane == 0) wait_counter(a.cnt2 + g, (unsigned)tm.sz, "pass-2 sums");
-        __syncwarp();
-        if (c < p.C) {
-          double tt[NV], sxs[K];
-#pragma unroll
-          for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
-#pragma unroll
-          for (int i = 0; i < K; ++i) sxs[i] = __ldcg(a.acc2 + ((size_t)g * K + i) * kCols + lane);
-          fold_channel<K, BWD>(a, c, in, tt, 0.0, 0.0, true, nullptr, sxs);
-        }
-      }
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
       printf("PSNTRACE %s fold cta %d total %llu cnt %llu fold %llu\n", BWD ? "bwd" : "fwd", (int)blockIdx.x,
@@ -829,7 +899,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = su32(smem) + (uint32_t)((n_in * kCols + lane) * sizeof(IO));  // this thread's column
   auto wait_item = [&]() -> uint32_t {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait(full + cs, cph);
+    mbar_wait(full + cs, cph, a.wait_ns);
     if (PSN_TRACE_BUILD && a.trace) {
       const unsigned long long dt = gtimer() - t0;
       tc_full += dt;
@@ -849,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto take_params = [&](int j) -> const unsigned char* {  // j: team-local group index
     const int sl = j & 1;
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    mbar_wait(p2f + sl, (unsigned)((j >> 1) & 1));
+    mbar_wait(p2f + sl, (unsigned)((j >> 1) & 1), a.wait_ns);
     if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
     return p2s + sl * LY.pbytes + lane * LY.pstride;
   };
@@ -861,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (the low warp stores, the high warp adds in fixed order and arrives)
   auto deposit = [&](const double* acc, int nv) {
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1));
+    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1), a.wait_ns);
     if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
     const int sw = warp & 7;
     if (warp < 8) {
@@ -885,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // pass-1 parameters of local group j (W and the moment shift, or the
   // forward's w_q and b_f): staged in shared memory by the publisher warp
   auto take_p1 = [&](int j) -> const double* {
-    mbar_wait(p1f + (j & 1), (unsigned)((j >> 1) & 1));
+    mbar_wait(p1f + (j & 1), (unsigned)((j >> 1) & 1), a.wait_ns);
     return (const double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
   };
   auto done_p1 = [&](int j) {
@@ -912,8 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!BWD) {
         // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
         constexpr int U = PSN_U_F1;
-        double w[K], xw[H + U], sh;
-#pragma unroll
+        double w[K], xw[H + U], sh, sxa = 0.0;
         {
           const double* pp = take_p1(it);
           for (int i = 0; i < K; ++i) w[i] = ldsd(pp + i);
@@ -963,6 +1032,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
                 S1[u] += hc;
                 S2[u] = fma(hc, hc, S2[u]);
+                // BN-term data sums of the backward's dW: P_i += x[t-off_i] (h1[t] - shift)
+                // (exact products, f64 sums; padding lanes and rows >= T see x = 0 / hc = 0)
+#pragma unroll
+                for (int i = 0; i < K; ++i) acc[2 + i] = fma(xw[u + slot<K, D>(i)], hc, acc[2 + i]);
+                sxa += xw[H + u];
               }
 #pragma unroll
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
@@ -977,6 +1051,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           release_item();
+          if constexpr (H > 0) {
+            // end of the stream: Sx_i = sum_{t < T - off_i} x[t] drops the last off_i
+            // samples of the stream (loaded from global: H values once per stream)
+            if (tt == p.ttl - 1 && lv) {
+              const IO* xp = (const IO*)a.x + (size_t)(nbi * kBoxN + n_in) * p.J + col;
+#pragma unroll
+              for (int r = 0; r < H; ++r) {
+                const int t = p.T - 1 - r;
+                const double v = t >= 0 ? (double)ld_io(xp + (size_t)t * rowstride) : 0.0;
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                  if (r < (K - 1 - i) * D) acc[2 + K + i] -= v;
+              }
+            }
+          }
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
@@ -984,11 +1073,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[2 + K + i] += sxa;  // sxa: sum of x over this thread's rows
       } else {
         // ---- backward pass 1: db, dw_q -- f64 end to end (h2 exact and f32-rounded like the
         // reference's carrier, sigma' and dh2 in f64): f32 per-element errors (~1e-7) would
         // grow to ~sqrt(m)*1e-7 in these m-term sums, above the 1e-5 bound on small dW
-        // entries.  (The BN term of dW is summed in pass 2.)  Rows
+        // entries.  (The BN term of dW comes from the forward's data sums.)  Rows
         // alternate between two f64 accumulator sets (ILP).
         constexpr int U = PSN_U_B1;
         double wq[K], xd[H + U], acc2[1 + K];
@@ -1150,8 +1241,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
         // partial dx of row t_blk - H + j; after a block of U rows the first U slots
-        // are complete).  Also forms the BN term of dW (network.py:298-315),
-        // sum_t x[t-off_i] dh1[t], f32 per tile and f64 across tiles.
+        // are complete).  The BN term of dW comes from the forward's exact data
+        // sums (fold_channel), so this pass only writes dx.
         constexpr int U = PSN_U_B2;
         float w[K], wq[K], xw[H + U], pacc[H + U];
         const double* pd = (const double*)pr;
@@ -1164,8 +1255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           wq[i] = (float)ldsd(pd + i);
           w[i] = ldsf(pf + i);
         }
-        const float bf = (float)ldsd(pd + K);
-        const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);
+        const float bf = (float)ldsd(pd + K);  // b_f + c sum w_q   (centred inputs, fold_channel)
+        const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);  // mu - c sum W
+        const float cx = ldsf(pf + K + 3);
         float wqs[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) wqs[i] = wq[i] * a.sur.scale;
@@ -1176,12 +1268,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto emit = [&](int od, float val) {
           if (lv && od >= run_t0 && od < p.T) st_out(out + (obase + (uint32_t)od * rs32), val, pol_out);
         };
-        double sacc[kMaxNV];
-#pragma unroll
-        for (int i = 0; i < kMaxNV; ++i) sacc[i] = 0.0;
-        float fsd[K];
         // dh2 / scale and dh1 of row u of the window (rows with !ok contribute nothing)
-        auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1, bool sum) {
+        auto dh_row = [&](int u, float yv, bool ok, float& dh2, float& dh1) {
           float h1c = fmaf(w[0], xw[u + slot<K, D>(0)], -mu), h2 = fmaf(wq[0], xw[u + slot<K, D>(0)], bf);
 #pragma unroll
           for (int i = 1; i < K; ++i) {
@@ -1191,10 +1279,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float r = rcp_approx(fmaf(cc * h2, h2, 1.0f));
           dh2 = ok ? yv * r : 0.f;
           dh1 = ok ? fmaf(b1, h1c, a1) : 0.f;
-          if (sum) {
-#pragma unroll
-            for (int i = 0; i < K; ++i) fsd[i] = fmaf(xw[u + slot<K, D>(i)], dh1, fsd[i]);
-          }
         };
         auto scatter = [&](int u, float dh2, float dh1) {
 #pragma unroll
@@ -1205,9 +1289,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // single-row step (TAIL rows): scatter, emit the row H behind, shift by one
         auto step1 = [&](float xv, float yv, bool ok, int tcur) {
-          xw[H] = xv;
+          xw[H] = xv - cx;
           float dh2, dh1;
-          dh_row(0, yv, ok, dh2, dh1, false);  // TAIL rows belong to the next range's sums
+          dh_row(0, yv, ok, dh2, dh1);
           scatter(0, dh2, dh1);
           emit(tcur - H, pacc[0]);
 #pragma unroll
@@ -1236,13 +1320,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             obase = (uint32_t)(lv ? n : 0) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
             run_t0 = t0;
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) xw[j] = pacc[j] = 0.f;
+            for (int j = 0; j < H + U; ++j) {
+              xw[j] = -cx;  // before the stream start: x = 0
+              pacc[j] = 0.f;
+            }
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = ldsx<IO>(xs + (r) * RSB);
+            for (int r = 0; r < H; ++r) xw[r] = ldsx<IO>(xs + (r) * RSB) - cx;
             release_item();
           }
           const uint32_t st = wait_item();
@@ -1256,10 +1343,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int r0 = 0; r0 < TB; r0 += U) {
                 float dh2[U], dh1[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
+                for (int u = 0; u < U; ++u) xw[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB) - cx;
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                  dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u], true);
+                  dh_row(u, ldsx<IO>(ys + ((r0 + u)) * RSB), FULL || r0 + u < nvalid, dh2[u], dh1[u]);
 #pragma unroll
                 for (int u = 0; u < U; ++u) scatter(u, dh2[u], dh1[u]);
                 const int od0 = t0 + r0 - H;  // rows od0 .. od0+U-1 are complete now
@@ -1287,11 +1374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
               }
             };
-#pragma unroll
-            for (int i = 0; i < K; ++i) fsd[i] = 0.f;
             if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
-#pragma unroll
-            for (int i = 0; i < K; ++i) sacc[i] += (double)fsd[i];
           }
           release_item();
           if constexpr (H > 0) {
@@ -1315,7 +1398,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           opaque(tt);
           opaque(nbi);
         }
-        if (v < tm.P && !(a.ablate & 16)) deposit(sacc, K);
       }
       if (PSN_TRACE_BUILD && a.trace) tc_pass[1] += gtimer() - tc_t;
     }
@@ -1331,6 +1413,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // -------------------------------------------------------------------------
 int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const void* dy, CUtensorMap* maps);
 
+// stream_launch result: the persistent kernel cannot be co-resident on this
+// device / context (occupancy, MPS or partition limits) -- run the generic path
+constexpr int kFallback = -1;
+
 template <int K, int D, typename IO, bool BWD>
 int stream_launch(const Args& args, const void* x, const void* dy, cudaStream_t st) {
   using C_ = Cfg<K, D, IO, BWD>;
@@ -1341,9 +1427,18 @@ int stream_launch(const Args& args, const void* x, const void* dy, cudaStream_t 
   auto kern = psn_stream_kernel<K, D, IO, BWD>;
   cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (stream kernel smem) failed");
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return kFallback;
+  }
   Args a = args;
   void* kargs[] = {(void*)&maps[0], (void*)&maps[1], (void*)&maps[2], (void*)&maps[3], (void*)&a};
   e = cudaLaunchCooperativeKernel((const void*)kern, dim3(args.p.nCTA), dim3(kThreads), kargs, smem, st);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();
+    return kFallback;
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     char buf[256];

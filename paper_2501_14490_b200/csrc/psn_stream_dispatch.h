@@ -12,6 +12,7 @@ int run_bf16_fwd(int k, int d, const Args& a, const void* x, const void* dy, cud
 int run_bf16_bwd(int k, int d, const Args& a, const void* x, const void* dy, cudaStream_t st);
 
 bool eligible(const psn_desc_t* desc);
+bool aligned_for_tma(const void* x, const void* dy);
 bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p);
 size_t workspace_bytes(const psn_desc_t* desc);
 int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* W, const double* gamma,

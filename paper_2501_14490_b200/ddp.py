@@ -50,6 +50,24 @@ class GradBucket:
         self.numels = [p.numel() for p in self.params]
         self.flat = torch.zeros(sum(self.numels), dtype=self.params[0].dtype, device=dev)
 
+    def views(self) -> list:
+        """Per-parameter views into the flat buffer, shaped like the parameters:
+        a backward that writes its gradients straight into them needs no pack
+        step before `reduce_()` (zero-copy bucket, as bench.py's step does)."""
+        out, off = [], 0
+        for p, n in zip(self.params, self.numels):
+            out.append(self.flat[off:off + n].view_as(p))
+            off += n
+        return out
+
+    def reduce_(self, group=None, average: bool = False) -> torch.Tensor:
+        """All-reduce the flat buffer in place (no pack / unpack)."""
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group)
+            if average:
+                self.flat.div_(dist.get_world_size(group))
+        return self.flat
+
     def pack(self) -> torch.Tensor:
         off = 0
         for p, n in zip(self.params, self.numels):
@@ -71,10 +89,7 @@ class GradBucket:
     def allreduce(self, group=None, average: bool = False) -> None:
         """Sum (or average) the bucket across the process group in place."""
         self.pack()
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group)
-            if average:
-                self.flat.div_(dist.get_world_size(group))
+        self.reduce_(group=group, average=average)
         self.unpack()
 
 

@@ -60,7 +60,7 @@ def quantize_pow2(w: torch.Tensor) -> ShiftWeights:
         raise ValueError("weights must be finite")
     sign = torch.empty(w.shape, dtype=torch.int8, device=w.device)
     expo = torch.empty(w.shape, dtype=torch.int8, device=w.device)
-    L.check(L.lib().psn_quantize_pow2(L.ptr(w), w.numel(), L.ptr(sign), L.ptr(expo), L.stream_of(w)))
+    L.run(w, "psn_quantize_pow2", L.ptr(w), w.numel(), L.ptr(sign), L.ptr(expo), L.stream_of(w))
     return ShiftWeights(sign, expo)
 
 
@@ -113,15 +113,15 @@ def conv_forward(x: torch.Tensor, w, bias=None, d: int = 1) -> torch.Tensor:
         b = _bias(bias, C, x.device)
         desc = L.make_desc(x.shape, sign.shape[1], d, x.dtype)
         out = torch.empty_like(x)
-        L.check(L.lib().psn_conv_forward_shift(ctypes.byref(desc), L.ptr(x), L.ptr(sign), L.ptr(expo),
-                                               sign.shape[0], L.ptr(b), L.ptr(out), L.stream_of(x)))
+        L.run(x, "psn_conv_forward_shift", ctypes.byref(desc), L.ptr(x), L.ptr(sign), L.ptr(expo),
+                                               sign.shape[0], L.ptr(b), L.ptr(out), L.stream_of(x))
         return out
     wv = _weights(w, C).to(x.device)
     b = _bias(bias, C, x.device)
     desc = L.make_desc(x.shape, wv.shape[1], d, x.dtype)
     out = torch.empty_like(x)
-    L.check(L.lib().psn_conv_forward(ctypes.byref(desc), L.ptr(x), L.ptr(wv), wv.shape[0], L.ptr(b),
-                                     L.ptr(out), L.stream_of(x)))
+    L.run(x, "psn_conv_forward", ctypes.byref(desc), L.ptr(x), L.ptr(wv), wv.shape[0], L.ptr(b),
+                                     L.ptr(out), L.stream_of(x))
     return out
 
 
@@ -150,9 +150,9 @@ def conv_forward_shift_int(x: torch.Tensor, w: ShiftWeights, bias=None, d: int =
     desc = L.make_desc(x.shape, sign.shape[1], d, torch.int32)
     out = torch.empty_like(x)
     sat = torch.zeros(1, dtype=torch.int64, device=x.device)
-    L.check(L.lib().psn_conv_forward_shift_int(ctypes.byref(desc), L.ptr(x), L.ptr(sign), L.ptr(expo),
+    L.run(x, "psn_conv_forward_shift_int", ctypes.byref(desc), L.ptr(x), L.ptr(sign), L.ptr(expo),
                                                sign.shape[0], L.ptr(b), L.ptr(out), L.ptr(sat),
-                                               L.stream_of(x)))
+                                               L.stream_of(x))
     return out, int(sat.item())
 
 
@@ -164,8 +164,8 @@ def conv_backward_input(dh: torch.Tensor, w, d: int = 1) -> torch.Tensor:
     wv = _weights(w, dh.shape[2]).to(dh.device)
     desc = L.make_desc(dh.shape, wv.shape[1], d, dh.dtype)
     out = torch.empty_like(dh)
-    L.check(L.lib().psn_conv_backward_input(ctypes.byref(desc), L.ptr(dh), L.ptr(wv), wv.shape[0],
-                                            L.ptr(out), L.stream_of(dh)))
+    L.run(dh, "psn_conv_backward_input", ctypes.byref(desc), L.ptr(dh), L.ptr(wv), wv.shape[0],
+                                            L.ptr(out), L.stream_of(dh))
     return out
 
 
@@ -183,8 +183,8 @@ def conv_backward_weight(x: torch.Tensor, dh: torch.Tensor, k: int, d: int = 1,
     desc = L.make_desc(x.shape, k, d, dt)
     grad = torch.empty((1 if shared else x.shape[2], k), dtype=torch.float64, device=x.device)
     ws = L.workspace(desc, x.device)
-    L.check(L.lib().psn_conv_backward_weight(ctypes.byref(desc), L.ptr(x), L.ptr(dh), int(bool(shared)),
-                                             L.ptr(grad), L.ptr(ws), L.stream_of(x)))
+    L.run(x, "psn_conv_backward_weight", ctypes.byref(desc), L.ptr(x), L.ptr(dh), int(bool(shared)),
+                                             L.ptr(grad), L.ptr(ws), L.stream_of(x))
     return grad
 
 
@@ -194,6 +194,6 @@ def conv_backward_bias(dh: torch.Tensor) -> torch.Tensor:
     desc = L.make_desc(dh.shape, 1, 1, dh.dtype)
     grad = torch.empty(dh.shape[2], dtype=torch.float64, device=dh.device)
     ws = L.workspace(desc, dh.device)
-    L.check(L.lib().psn_conv_backward_bias(ctypes.byref(desc), L.ptr(dh), L.ptr(grad), L.ptr(ws),
-                                           L.stream_of(dh)))
+    L.run(dh, "psn_conv_backward_bias", ctypes.byref(desc), L.ptr(dh), L.ptr(grad), L.ptr(ws),
+                                           L.stream_of(dh))
     return grad

@@ -51,13 +51,12 @@ class _PSNFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, W, gamma, beta, running_mean, running_var, desc_args, layer):
         desc = L.make_desc(x.shape, *desc_args)
-        lib = L.lib()
         out = torch.empty_like(x)
-        fold = torch.empty((x.shape[2], L.PSN_FOLD_HDR + 2 * desc.k), dtype=torch.float64, device=x.device)
+        fold = torch.empty((x.shape[2], L.fold_stride(desc.k)), dtype=torch.float64, device=x.device)
         ws = L.workspace_for(desc, x.device, L.stream_of(x))
-        L.check(lib.psn_forward_train(ctypes.byref(desc), L.ptr(x), L.ptr(W), L.ptr(gamma), L.ptr(beta),
+        L.run(x, "psn_forward_train", ctypes.byref(desc), L.ptr(x), L.ptr(W), L.ptr(gamma), L.ptr(beta),
                                       L.ptr(running_mean), L.ptr(running_var), L.ptr(out), L.ptr(fold),
-                                      L.ptr(ws), L.stream_of(x)))
+                                      L.ptr(ws), L.stream_of(x))
         ctx.save_for_backward(x, W, gamma, fold)
         ctx.desc_args = desc_args
         if layer is not None:
@@ -74,9 +73,9 @@ class _PSNFunction(torch.autograd.Function):
         dgamma = torch.empty_like(gamma)
         dbeta = torch.empty_like(gamma)
         ws = L.workspace_for(desc, x.device, L.stream_of(x))
-        L.check(L.lib().psn_backward(ctypes.byref(desc), L.ptr(x), L.ptr(dy), L.ptr(W), L.ptr(gamma),
+        L.run(x, "psn_backward", ctypes.byref(desc), L.ptr(x), L.ptr(dy), L.ptr(W), L.ptr(gamma),
                                      L.ptr(fold), L.ptr(dx), L.ptr(dW), L.ptr(dgamma), L.ptr(dbeta),
-                                     L.ptr(ws), L.stream_of(x)))
+                                     L.ptr(ws), L.stream_of(x))
         return dx, dW, dgamma, dbeta, None, None, None, None
 
 
@@ -137,6 +136,8 @@ class SpikingLayer(nn.Module):
         if x.shape[2] != self.cfg.channels:
             raise ValueError(f"input has {x.shape[2]} channels, config expects {self.cfg.channels}")
         if x.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+            # the reference's TemporalTensor converts any other dtype to float64
+            # (tensor.py:17, 57-59), and its outputs then carry float64 too
             x = x.to(torch.float64)
         return x.contiguous()
 
@@ -171,14 +172,15 @@ class SpikingLayer(nn.Module):
         out = torch.empty_like(x)
         ws = L.workspace(desc, x.device)
         with torch.no_grad():
-            L.check(L.lib().psn_forward_eval(ctypes.byref(desc), L.ptr(x), L.ptr(self.W), L.ptr(self.gamma),
+            L.run(x, "psn_forward_eval", ctypes.byref(desc), L.ptr(x), L.ptr(self.W), L.ptr(self.gamma),
                                              L.ptr(self.beta), L.ptr(self.running_mean),
-                                             L.ptr(self.running_var), L.ptr(out), L.ptr(ws), L.stream_of(x)))
+                                             L.ptr(self.running_var), L.ptr(out), L.ptr(ws), L.stream_of(x))
         return out
 
     # -- inspection of the last TRAIN/SMOOTH forward (the reference's _cache) ---
     def last_state(self) -> dict:
-        """mu*, s, a, b_f, batch mean/var, w_f, w_q of the last forward."""
+        """mu*, s, a, b_f, batch mean/var, w_f, w_q of the last forward, and (streamed
+        forward) the BN-term data sums sx, cx the backward's dW uses."""
         f = self.last_fold
         if f is None:
             raise RuntimeError("no forward has run yet")
@@ -186,7 +188,9 @@ class SpikingLayer(nn.Module):
         return {"mu": f[:, 0], "s": f[:, 1], "a": f[:, 2], "b_f": f[:, 3],
                 "mu_batch": f[:, 4], "var_batch": f[:, 5],
                 "w_f": f[:, L.PSN_FOLD_HDR:L.PSN_FOLD_HDR + k],
-                "w_q": f[:, L.PSN_FOLD_HDR + k:L.PSN_FOLD_HDR + 2 * k]}
+                "w_q": f[:, L.PSN_FOLD_HDR + k:L.PSN_FOLD_HDR + 2 * k],
+                "sx": f[:, L.PSN_FOLD_HDR + 2 * k:L.PSN_FOLD_HDR + 3 * k],
+                "cx": f[:, L.PSN_FOLD_HDR + 3 * k:L.PSN_FOLD_HDR + 4 * k]}
 
 
 class ShiftLayer(nn.Module):

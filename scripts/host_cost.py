@@ -9,7 +9,7 @@ cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
 layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(1), device=dev)
 lib = L.lib(); desc = L.make_desc(x.shape, k, d, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
 ws = L.workspace(desc, dev); out = torch.empty_like(x); dx = torch.empty_like(x)
-fold = torch.empty((C, L.PSN_FOLD_HDR + 2*k), dtype=torch.float64, device=dev)
+fold = torch.empty((C, L.fold_stride(k)), dtype=torch.float64, device=dev)
 g = torch.empty(C*k+2*C, dtype=torch.float64, device=dev)
 sp = torch.cuda.current_stream().cuda_stream
 W, gam, bet, rm, rv = layer.W.detach(), layer.gamma.detach(), layer.beta.detach(), layer.running_mean, layer.running_var
