@@ -21,6 +21,8 @@
  *   psn_conv_backward_weight    engines.conv_backward_weight          engines.py:402-425
  *   psn_conv_backward_bias      engines.conv_backward_bias            engines.py:428-431
  *   psn_quantize_pow2           quant.quantize_pow2                   quant.py:111-139
+ *   psn_readout_reduce  ReadoutLayer.forward (leaky accumulator)      network.py:399-419
+ *   psn_readout_expand  ReadoutLayer.backward (dcur -> dx)            network.py:421-436
  *
  * Tensor layout: time-first, contiguous [T, N, C, Q] where Q is the product of
  * the spatial axes (1 for rank-3 [T, N, C]); reference tensor.py:71-81.
@@ -165,6 +167,18 @@ PSN_API int psn_conv_backward_bias(const psn_desc_t *desc, const void *dh, doubl
 /* n float64 weights -> int8 sign / exponent (exact nearest pow2, clamp [-16, 15]) */
 PSN_API int psn_quantize_pow2(const double *w, int64_t n, int8_t *sign, int8_t *exponent,
                       psn_stream_t stream);
+
+/* ---- readout leaky accumulator (network.py:365-436) --------------------- */
+/* The readout's v = (1 - 1/tau) v + (1/tau) cur[t] over t, with the linear
+ * cur[t] = x[t] W^T + b, equals xbar W^T + b sum_t w_t with
+ *   xbar[n, c] = sum_t w_t x[t, n, c],  w_t = (1/tau) (1 - 1/tau)^(T-1-t).
+ * psn_readout_reduce: x [T, N, C] (dtype f32 / bf16 / f64) -> xbar [N, C] f64.
+ * psn_readout_expand: backward, dx[t, n, c] = w_t g[n, c] for g = dlogits W
+ *   ([N, C] f64) -> dx [T, N, C] in dtype.  tau > 1 (else PSN_ERR_INVALID).  */
+PSN_API int psn_readout_reduce(int64_t T, int64_t N, int64_t C, int32_t dtype, double tau,
+                               const void *x, double *xbar, psn_stream_t stream);
+PSN_API int psn_readout_expand(int64_t T, int64_t N, int64_t C, int32_t dtype, double tau,
+                               const double *g, void *dx, psn_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,7 @@ EXPORTED = (
     "psn_workspace_bytes", "psn_forward_train", "psn_backward", "psn_forward_eval",
     "psn_conv_forward", "psn_conv_forward_shift", "psn_conv_forward_shift_int",
     "psn_conv_backward_input", "psn_conv_backward_weight", "psn_conv_backward_bias",
-    "psn_quantize_pow2", "psn_plan_info",
+    "psn_quantize_pow2", "psn_plan_info", "psn_readout_reduce", "psn_readout_expand",
 )
 
 
@@ -70,6 +70,10 @@ _SIGS = {
     "psn_conv_backward_bias": (ctypes.c_int, [_D, _P, _P, _P, _P]),
     "psn_quantize_pow2": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P, _P]),
     "psn_plan_info": (ctypes.c_int, [_D, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
+    "psn_readout_reduce": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_double, _P, _P, _P]),
+    "psn_readout_expand": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_double, _P, _P, _P]),
 }
 
 _lib = None

@@ -105,7 +105,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   if (tpg * (long long)(g_sms + 1) >= (1LL << 32)) return false;  // 32-bit schedule arithmetic
   p.tpg = (int)tpg;
   p.nCTA = g_sms;
-  p.lag = env_int("PSN_LAG", 2);
+  p.lag = env_int(bwd ? "PSN_LAG_BWD" : "PSN_LAG_FWD", env_int("PSN_LAG", 2));
   if (p.lag < 1) p.lag = 1;
   if (p.lag > 6) p.lag = 6;  // the publisher's ring of pre-update running statistics holds 8 groups
   // CTA teams: nT teams stream nT groups concurrently, so each CTA's range of a
@@ -119,7 +119,7 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
     if (nT < 1) nT = 1;
     while (nT < p.G && p.G % nT != 0) ++nT;
     if (nT > p.G) nT = p.G;
-    nT = env_int("PSN_TEAMS", nT);
+    nT = env_int(bwd ? "PSN_TEAMS_BWD" : "PSN_TEAMS_FWD", env_int("PSN_TEAMS", nT));
     if (nT < 1) nT = 1;
     if (nT > p.G) nT = p.G;
     if (nT > p.nCTA) nT = p.nCTA;

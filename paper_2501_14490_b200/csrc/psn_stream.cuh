@@ -277,7 +277,11 @@ __device__ __forceinline__ float ldsf(const float* p) {
 // normal.  In the f32 denormal range (|h| < 2^-126) it keeps extra bits: that
 // cannot change sigma'(h) = 1 / (1 + c h^2) (1.0 exactly there), and moves a
 // moment sum by < 2^-149 per element.
+#ifndef PSN_ROUND_CVT
+#define PSN_ROUND_CVT 0  // 1: round with F2F.F32.F64 + F2F.F64.F32 instead (A/B experiment)
+#endif
 __device__ __forceinline__ double round_f32_sg(double h) {
+  if (PSN_ROUND_CVT) return (double)__double2float_rn(h);
   const unsigned long long b = (unsigned long long)__double_as_longlong(h);
   const unsigned long long r = (b + 0x0FFFFFFFull + ((b >> 29) & 1ull)) & ~0x1FFFFFFFull;
   return __longlong_as_double((long long)r);

@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = L.lib()
     for name in _declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.psn_abi_version() == 1
+    assert lib.psn_abi_version() == 2
     assert lib.psn_max_order() == L.PSN_MAX_ORDER_PY
 
 
@@ -42,7 +42,7 @@ def test_workspace_and_fold_sizes():
     from paper_2501_14490_b200 import _lib as L
     lib = L.lib()
     d = L.make_desc((1024, 64, 512), 4, 1, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
-    assert lib.psn_fold_doubles(ctypes.byref(d)) == 512 * (6 + 8)
+    assert lib.psn_fold_doubles(ctypes.byref(d)) == 512 * (7 + 4 * 4) == 512 * L.fold_stride(4)
     ws = lib.psn_workspace_bytes(ctypes.byref(d))
     assert 0 < ws < 64 << 20
     bad = L.make_desc((4, 2, 3), 17, 1, torch.float32)

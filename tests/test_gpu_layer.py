@@ -130,9 +130,9 @@ def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0, s
     gdx = x.grad.float().cpu().numpy()[:, :, sel]
     if dtype == torch.float32:
         assert_close_scaled(gdx, dx, 1e-5, "dx")
-    else:  # bf16 dx: the f32 result rounded to bf16 (half an ulp = 2^-9 relative) + the f32 bound
+    else:  # bf16 dx: the f32 result rounded to bf16 (half an ulp <= 2^-8 |dx|) + the f32 bound
         err = np.abs(gdx.astype(np.float64) - dx)
-        bound = 2.0 ** -9 * np.abs(dx) + 1e-5 * np.maximum(np.abs(dx), 1.0)
+        bound = 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(np.abs(dx), 1.0)
         assert not (err > bound).any(), f"bf16 dx: {int((err > bound).sum())} outside; max err {err.max():.3e}"
     assert_close_scaled(layer.W.grad.cpu().numpy()[sel], dW, 1e-5, "dW")
     assert_close_scaled(layer.gamma.grad.cpu().numpy()[sel], dg, 1e-5, "dgamma")

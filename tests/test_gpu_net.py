@@ -1,0 +1,209 @@
+"""GPU parity of the full training step around the neuron (SURVEY.md section
+8(f) rank 2) and of quantized export (rank 3) against fixtures the reference
+wrote (tests/golden/make_golden_net.py): SpikingNet.train_step_grads with the
+reference's Adam, two steps; EVAL logits; SSNN1 files of the trained net."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from tests.parity import assert_close_scaled, assert_rel
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _z():
+    return np.load(os.path.join(GOLDEN, "net_train.npz"))
+
+
+def _net(dtype=torch.float64):
+    from paper_2501_14490_b200.net import build_task_net
+    T, N, IN, CH, CLASSES, ORDER, SEED = (int(v) for v in _z()["meta"])
+    return build_task_net(channels=CH, num_layers=3, order=ORDER, classes=CLASSES, seed=SEED,
+                          in_features=IN, device="cuda")
+
+
+def _train_two_steps(net, dtype=torch.float64):
+    from paper_2501_14490_b200.net import Adam
+    z = _z()
+    params = net.parameters_list()
+    opt = Adam(params, float(z["lr"]))
+    res = []
+    for step in range(2):
+        x = torch.tensor(z[f"s{step}_x"], device="cuda", dtype=dtype)
+        y = torch.tensor(z[f"s{step}_y"], device="cuda")
+        loss, acc = net.train_step_grads(x, y)
+        grads = [p.grad.detach().cpu().numpy().copy() for p in params]
+        stats = [(l.running_mean.cpu().numpy().copy(), l.running_var.cpu().numpy().copy())
+                 for l in net.spiking_layers()]
+        opt.step()
+        res.append((loss, acc, grads, stats, [p.detach().cpu().numpy().copy() for p in params]))
+    return res
+
+
+def test_training_step_matches_reference_f64():
+    """float64 carrier: the reference's TRAIN arithmetic (Linear, PSN layers on
+    the generic f64 kernels, readout, CE, Adam), two steps."""
+    z = _z()
+    net = _net()
+    for step, (loss, acc, grads, stats, after) in enumerate(_train_two_steps(net)):
+        assert abs(loss - float(z[f"s{step}_loss"])) <= 1e-12 * max(1.0, abs(float(z[f"s{step}_loss"])))
+        assert acc == float(z[f"s{step}_acc"])
+        for i, g in enumerate(grads):
+            assert_close_scaled(g, z[f"s{step}_grad_{i}"], 1e-9, f"step {step} grad {i}")
+        for j, (rm, rv) in enumerate(stats):
+            assert_rel(rm, z[f"s{step}_rm_{j}"], 1e-10, f"running_mean {j}")
+            assert_rel(rv, z[f"s{step}_rv_{j}"], 1e-10, f"running_var {j}")
+        for i, p in enumerate(after):
+            assert_close_scaled(p, z[f"s{step}_after_{i}"], 1e-9, f"step {step} param {i}")
+
+
+def test_eval_logits_and_predictions_match_reference():
+    from paper_2501_14490_b200.layer import Mode
+    z = _z()
+    net = _net()
+    _train_two_steps(net)
+    xe = torch.tensor(z["eval_x"], device="cuda")
+    logits = net(xe, Mode.EVAL).detach().double().cpu().numpy()
+    assert_close_scaled(logits, z["eval_logits"], 1e-5, "eval logits (f32 deployment path)")
+    assert np.array_equal(net.predict(xe).cpu().numpy(), z["eval_pred"])
+
+
+def test_quantized_export_matches_reference_file():
+    """quantized_snapshot (running stats folded, pow2-quantized on the GPU) of
+    the trained net gives the reference's sign / exponent bytes; the fused
+    f32 biases agree to an f32 ulp."""
+    from paper_2501_14490_b200 import modelio
+    net = _net()
+    _train_two_steps(net)
+    got = modelio.model_bytes(net, quantize=True)
+    want = open(os.path.join(GOLDEN, "ssnn1_quantized.bin"), "rb").read()
+    assert len(got) == len(want)
+    gnet, _ = modelio.model_from_bytes(got, device="cpu")
+    wnet, _ = modelio.model_from_bytes(want, device="cpu")
+    for a, b in zip(gnet.layers, wnet.layers):
+        assert type(a) is type(b)
+        if hasattr(a, "sw"):
+            assert torch.equal(a.sw.sign, b.sw.sign) and torch.equal(a.sw.exponent, b.sw.exponent)
+            assert a.dilation == b.dilation
+            assert_close_scaled(a.bias.numpy(), b.bias.numpy(), 2 ** -22, "fused bias")
+        else:
+            assert_close_scaled(a.W.detach().numpy(), b.W.detach().numpy(), 2 ** -22, "weights")
+
+
+def test_quantized_model_inference_matches_reference():
+    """The reference's quantized file reloads as ShiftLayers; the EVAL logits of
+    the mul-free network equal the reference's."""
+    from paper_2501_14490_b200 import modelio
+    from paper_2501_14490_b200.layer import Mode
+    z = _z()
+    qnet, meta = modelio.load_model(os.path.join(GOLDEN, "ssnn1_quantized.bin"), device="cuda")
+    assert meta["quantized"]
+    logits = qnet(torch.tensor(z["eval_x"], device="cuda"), Mode.EVAL).detach().double().cpu().numpy()
+    want = np.load(os.path.join(GOLDEN, "net_quantized_eval.npz"))["q_eval_logits"]
+    assert_close_scaled(logits, want, 1e-5, "quantized eval logits")
+
+
+def test_readout_kernels_against_reference_recurrence():
+    """psn_readout_reduce / _expand vs the reference's sequential leaky
+    accumulator (network.py:413-436) on random data, f32 / f64 / bf16 carriers."""
+    from paper_2501_14490_b200.net import ReadoutLayer
+    rng = np.random.default_rng(3)
+    for dt in (torch.float64, torch.float32, torch.bfloat16):
+        T, N, C, K = 37, 5, 11, 3
+        x = torch.tensor(rng.standard_normal((T, N, C)), device="cuda").to(dt)
+        ro = ReadoutLayer(C, K, tau=2.5, rng=np.random.default_rng(1), device="cuda")
+        xr = x.double().requires_grad_(True)
+        logits = ro(x.detach().requires_grad_(True) if dt != torch.float64 else xr)
+        xd = x.detach().double().cpu().numpy()
+        W, b = ro.W.detach().cpu().numpy(), ro.b.detach().cpu().numpy()
+        cur = np.einsum("tnc,oc->tno", xd, W) + b
+        inv = 1.0 / ro.tau
+        v = np.zeros_like(cur[0])
+        for t in range(T):
+            v = (1 - inv) * v + inv * cur[t]
+        assert_close_scaled(logits.detach().cpu().numpy(), v, 1e-12, f"logits {dt}")
+        g = rng.standard_normal((N, K))
+        xin = x.detach().clone().requires_grad_(True)
+        ro(xin).backward(torch.tensor(g, device="cuda"))
+        gg = g.copy()
+        dcur = np.empty((T, N, K))
+        for t in range(T - 1, -1, -1):
+            dcur[t] = inv * gg
+            gg = (1 - inv) * gg
+        dx = np.einsum("tno,oc->tnc", dcur, W)
+        tol = {torch.float64: 1e-12, torch.float32: 1e-6, torch.bfloat16: 2 ** -8}[dt]
+        assert_close_scaled(xin.grad.double().cpu().numpy(), dx, tol, f"dx {dt}")
+        assert_close_scaled(ro.W.grad.cpu().numpy(), np.einsum("tno,tnc->oc", dcur, xd), 1e-12, f"dW {dt}")
+
+
+def test_f32_network_trains_on_the_streamed_kernels():
+    """The production setting: f32 activations through the streamed PSN
+    kernels; the step runs, its loss tracks the f64 reference's, and training
+    reduces the loss on a fixed batch."""
+    from paper_2501_14490_b200.net import Adam
+    z = _z()
+    net = _net()
+    x = torch.tensor(z["s0_x"], device="cuda", dtype=torch.float32)
+    y = torch.tensor(z["s0_y"], device="cuda")
+    loss0, _ = net.train_step_grads(x, y)
+    assert abs(loss0 - float(z["s0_loss"])) < 1e-3
+    opt = Adam(net.parameters_list(), 1e-2)
+    for _ in range(30):
+        net.train_step_grads(x, y)
+        opt.step()
+    loss1, _ = net.train_step_grads(x, y)
+    assert loss1 < loss0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ddp_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from paper_2501_14490_b200 import ddp
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        z = _z()
+        net = _net()
+        x = torch.tensor(z["s0_x"], device="cuda")
+        y = torch.tensor(z["s0_y"], device="cuda")
+        a, b = ddp.shard_bounds(x.shape[1], rank, world)
+        net.train_step_grads(x[:, a:b].contiguous(), y[a:b])
+        bucket = ddp.GradBucket(net.parameters_list())
+        bucket.allreduce()
+        out[rank] = [p.grad.cpu().numpy().copy() for p in net.parameters_list()]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ddp_step_two_ranks_on_product_kernels():
+    """World size 2 (gloo, both ranks on cuda:0): each rank runs the product
+    kernels on its batch shard; the bucketed all-reduce gives the sum of the
+    per-shard gradients a single process computes."""
+    import torch.multiprocessing as mp
+    from paper_2501_14490_b200 import ddp
+    z = _z()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ddp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    x = torch.tensor(z["s0_x"], device="cuda")
+    y = torch.tensor(z["s0_y"], device="cuda")
+    want = None
+    for r in range(2):
+        net = _net()
+        a, b = ddp.shard_bounds(x.shape[1], r, 2)
+        net.train_step_grads(x[:, a:b].contiguous(), y[a:b])
+        g = [p.grad.cpu().numpy() for p in net.parameters_list()]
+        want = g if want is None else [u + v for u, v in zip(want, g)]
+    for r in range(2):
+        for got, w in zip(out[r], want):
+            np.testing.assert_allclose(got, w, rtol=1e-12, atol=1e-14)
