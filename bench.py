@@ -203,16 +203,19 @@ class Workload:
     """One rank's share of the neuron layer step, driven through the C ABI:
     spikes/dx and a GradBucket whose views receive dW, dgamma, dbeta."""
 
-    def __init__(self, P, L, dev, T, Bl, C, k, d, dt, seed, use_graph):
+    def __init__(self, P, L, dev, shape, k, d, dt, seed, use_graph):
         import numpy as np
         import torch
         from paper_2501_14490_b200 import ddp
         self.torch, self.L = torch, L
-        self.nel = T * Bl * C
+        C = shape[2]
+        self.nel = 1
+        for s_ in shape:
+            self.nel *= s_
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
-        self.x = torch.randn((T, Bl, C), generator=g, device=dev).to(dt)
-        self.dy = torch.randn((T, Bl, C), generator=g, device=dev).to(dt)
+        self.x = torch.randn(shape, generator=g, device=dev).to(dt)
+        self.dy = torch.randn(shape, generator=g, device=dev).to(dt)
         cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
         self.layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(1), device=dev)
         flags = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
@@ -302,6 +305,73 @@ class Workload:
         f = [evd[3 * i].elapsed_time(evd[3 * i + 1]) for i in range(K)]
         b = [evd[3 * i + 1].elapsed_time(evd[3 * i + 2]) for i in range(K)]
         return statistics.mean(f), statistics.mean(b)
+
+
+SUITE = [
+    # (name, shape [T, B, C, *spatial], k, d, dtype): BASELINE.json configs, SURVEY.md section 8(d) inputs
+    ("cfg1_T250_B32_C128_k4_d1", (250, 32, 128), 4, 1, "f32"),
+    ("cfg1_T250_B32_C128_k4_d2", (250, 32, 128), 4, 2, "f32"),
+    ("cfg1_T250_B32_C128_k4_d3", (250, 32, 128), 4, 3, "f32"),
+    ("shard8_T1024_B8_C512_k4_d1", (1024, 8, 512), 4, 1, "f32"),
+    ("seqcifar_T32_B128_C128x32_k16", (32, 128, 128, 32), 16, 1, "f32"),
+    ("seqcifar_fc_T32_B128_C256_k16", (32, 128, 256), 16, 1, "f32"),
+    ("dvslip_T30_B32_C64x22x22_k2_bf16", (30, 32, 64, 22, 22), 2, 1, "bf16"),
+    ("dvslip_T30_B32_C512x3x3_k2_bf16", (30, 32, 512, 3, 3), 2, 2, "bf16"),
+    ("sweep_T1024_k4_bf16", (1024, 64, 512), 4, 1, "bf16"),
+    ("sweep_T1024_k8_d3", (1024, 64, 512), 8, 3, "f32"),
+    ("sweep_T1024_k16_d3", (1024, 64, 512), 16, 3, "f32"),
+    ("sweep_T4096_k4", (4096, 64, 512), 4, 1, "f32"),
+    ("sweep_T16384_k4", (16384, 64, 512), 4, 1, "f32"),
+]
+
+
+def run_suite(P, L, dev, hbm, m=3):
+    """Every BASELINE config on one GPU, timed with the 2m+1 / last-m protocol
+    (paper_2501_14490_b200.protocol): per neuron layer shape fwd+bwd through
+    the C ABI (CUDA-graph replay), and the SHD-shaped 3-layer full training
+    step (Linear 700->128 and 128->128, PSN layers k and sawtooth d, readout,
+    CE, Adam) through the module API."""
+    import numpy as np
+    import torch
+    from paper_2501_14490_b200 import protocol
+    from paper_2501_14490_b200.net import Adam, GraphedTrainStep, build_task_net
+    out = {}
+    for name, shape, k, d, dts in SUITE:
+        dt = torch.float32 if dts == "f32" else torch.bfloat16
+        try:
+            wl = Workload(P, L, dev, shape, k, d, dt, 99, True)
+            sec = protocol.benchmark_candidate(wl.run_s, m=m)
+            es = 4 if dts == "f32" else 2
+            out[name] = {"shape": list(shape), "k": k, "d": d, "dtype": dts, "ms": sec * 1e3,
+                         "gsteps_ch_per_s": wl.nel / sec / 1e9,
+                         "hbm_frac": 5 * es * wl.nel / sec / 1e9 / hbm,
+                         "streamed": [wl.plan_f.get("streamed"), wl.plan_b.get("streamed")]}
+            del wl
+        except Exception as e:  # a config that cannot run is reported, not fatal
+            out[name] = {"error": str(e)[:200]}
+        torch.cuda.empty_cache()
+    for korder in (2, 4):
+        T, B, IN, H = 250, 128, 700, 128
+        net = build_task_net(channels=H, num_layers=3, order=korder, classes=20, seed=0, in_features=IN,
+                             device=dev)
+        g = torch.Generator(device=dev).manual_seed(5)
+        x = (torch.rand((T, B, IN), generator=g, device=dev) < 0.05).to(torch.float32)
+        y = torch.randint(0, 20, (B,), generator=g, device=dev)
+        opt = Adam(net.parameters_list(), 1e-3)
+
+        def step():
+            net.train_step_grads_async(x, y)
+            opt.step()
+        sec_eager = protocol.benchmark_candidate(step, m=m)
+        graphed = GraphedTrainStep(net, opt, x, y)
+        sec = protocol.benchmark_candidate(graphed, m=m)
+        out[f"shd_train_step_T250_B128_in700_h128_k{korder}"] = {
+            "ms": sec * 1e3, "ms_eager": sec_eager * 1e3, "samples_per_s": B / sec,
+            "neuron_gsteps_ch_per_s": 3 * T * B * H / sec / 1e9,
+            "what": "3 x (Linear + PSN layer, sawtooth d=1,2,3) + readout + CE + Adam, f32 activations; "
+                    "one CUDA graph per step (GraphedTrainStep); ms_eager = the same step launched eagerly"}
+        del net, opt, graphed
+    return out
 
 
 def max_over_ranks(v, world, dist, dev):
@@ -408,6 +478,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-weak", action="store_true", help="N>1: skip the extra weak-scaling measurement")
+    ap.add_argument("--no-suite", action="store_true", help="skip the per-config suite (BASELINE configs 1-5)")
     ap.add_argument("--no-graph", action="store_true", help="time direct C-ABI calls instead of CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -443,7 +514,7 @@ def main():
     dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     esize = 4 if dt == torch.float32 else 2
     Bl, Bg = batch_shard(args.B, rank, world, args.scaling)
-    wl = Workload(P, L, dev, T, Bl, C, k, d, dt, 1234 + rank, not args.no_graph)
+    wl = Workload(P, L, dev, (T, Bl, C), k, d, dt, 1234 + rank, not args.no_graph)
     K = args.steps
 
     with ClockSampler(dev.index) as clk:
@@ -458,7 +529,7 @@ def main():
     if world > 1 and not args.no_weak:
         other = "weak" if args.scaling == "strong" else "strong"
         Bl2, Bg2 = batch_shard(args.B, rank, world, other)
-        wl2 = Workload(P, L, dev, T, Bl2, C, k, d, dt, 4321 + rank, not args.no_graph)
+        wl2 = Workload(P, L, dev, (T, Bl2, C), k, d, dt, 4321 + rank, not args.no_graph)
         ms2 = max_over_ranks(wl2.time_steps(K, args.warmup, world, dist), world, dist, dev)
         weak = {"scaling": other, "value": T * Bg2 * C / (ms2 * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms2,
                 "B_per_gpu": Bl2, "global_batch": Bg2}
@@ -487,6 +558,10 @@ def main():
     if not args.no_e2e:
         e = run_e2e(P, wl, world, dist, K)
         e2e = {"value": T * Bg * C / (e["ms_per_step"] * 1e-3) / 1e9, "unit": UNIT, **e}
+
+    suite = None
+    if rank == 0 and world == 1 and not args.no_suite:
+        suite = run_suite(P, L, dev, _peaks()[0])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -523,6 +598,8 @@ def main():
         }
         if weak is not None:
             line["weak"] = weak
+        if suite is not None:
+            line["suite"] = suite
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

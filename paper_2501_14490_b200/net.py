@@ -204,11 +204,25 @@ class Adam:
         self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
         self.t = 0
         self._state = {}
+        self._t_dev = None  # capturable mode: the step count lives on the device
+
+    def make_capturable(self) -> None:
+        """Keep the step count on the device so a captured step (CUDA graph)
+        advances the bias corrections on every replay; the corrections are then
+        1 - beta^t from the device pow (within an ulp of the host's)."""
+        if self._t_dev is None:
+            self._t_dev = torch.full((), float(self.t), dtype=torch.float64, device=self.params[0].device)
 
     @torch.no_grad()
     def step(self) -> None:
         self.t += 1
         b1, b2 = self.beta1, self.beta2
+        if self._t_dev is not None:
+            self._t_dev.add_(1.0)
+            c1 = 1 - torch.pow(b1, self._t_dev)
+            c2 = 1 - torch.pow(b2, self._t_dev)
+        else:
+            c1, c2 = 1 - b1 ** self.t, 1 - b2 ** self.t
         for p in self.params:
             st = self._state.get(id(p))
             if st is None:
@@ -219,9 +233,40 @@ class Adam:
             m.add_((1 - b1) * g)
             v.mul_(b2)
             v.add_((1 - b2) * g * g)
-            mh = m / (1 - b1 ** self.t)
-            vh = v / (1 - b2 ** self.t)
+            mh = m / c1
+            vh = v / c2
             p.sub_(self.lr * mh / (torch.sqrt(vh) + self.eps))
+
+
+class GraphedTrainStep:
+    """One training step (zero_grad, forward, cross entropy, backward,
+    optimizer update) captured into a CUDA graph and replayed on static
+    input / label buffers: the step is then one graph launch instead of a few
+    hundred small kernel launches (the C-ABI calls are stream-ordered and
+    allocation-free, so they capture).  Use: ``step = GraphedTrainStep(net,
+    opt, x, y)``; copy the next batch into ``step.x`` / ``step.y``;
+    ``loss, acc = step()`` (device tensors, no host synchronisation)."""
+
+    def __init__(self, net: SpikingNet, opt, x: torch.Tensor, labels: torch.Tensor, warmup: int = 3):
+        self.net, self.opt = net, opt
+        if hasattr(opt, "make_capturable"):
+            opt.make_capturable()
+        self.x, self.y = x.clone(), labels.clone()
+        side = torch.cuda.Stream(x.device)
+        side.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.stream(side):  # warm-up (workspaces, grads, optimizer state) off the capture
+            for _ in range(warmup):
+                net.train_step_grads_async(self.x, self.y)
+                opt.step()
+        torch.cuda.current_stream(x.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss, self.acc = net.train_step_grads_async(self.x, self.y)
+            opt.step()
+
+    def __call__(self):
+        self.graph.replay()
+        return self.loss, self.acc
 
 
 def build_task_net(channels: int = 24, num_layers: int = 3, order: int = 2,
@@ -258,4 +303,4 @@ def _device(device):
 
 
 __all__ = ["LinearLayer", "ReadoutLayer", "ShiftLayer", "SpikingNet", "ce_loss", "SGD", "Adam",
-           "build_task_net"]
+           "GraphedTrainStep", "build_task_net"]

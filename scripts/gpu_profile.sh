@@ -4,7 +4,7 @@
 TAG=${1:-prof}; shift
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-BARGS="--steps 2 --warmup 3 --no-cpu-baseline --no-e2e $*"
+BARGS="--steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-suite $*"
 if [ -n "$MICROBENCH" ]; then
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb scripts/microbench_pipes.cu && timeout 60 /tmp/mb > $OUT/microbench.txt 2>&1
 fi

@@ -4,7 +4,7 @@
 TAG=$1; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 for cfg in "$@"; do
-  env $cfg timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e $BENCH_ARGS > $OUT/tmp.json 2>$OUT/tmp.err
+  env $cfg timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-suite $BENCH_ARGS > $OUT/tmp.json 2>$OUT/tmp.err
   python - "$cfg" $OUT/tmp.json <<'PY' >> $OUT/sweep.txt
 import json,sys
 try:

@@ -7,7 +7,7 @@ OUT=gpurun_out/$TAG; mkdir -p $OUT; : > $OUT/variants.txt
 for rep in 1 2; do
   for v in base "$@"; do
     lib=""; [ $v != base ] && lib=$PWD/paper_2501_14490_b200/_lib_$v/libpsn_b200.so
-    PSN_B200_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $OUT/tmp.json 2>$OUT/tmp.err
+    PSN_B200_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-suite > $OUT/tmp.json 2>$OUT/tmp.err
     python - $v $OUT/tmp.json >> $OUT/variants.txt <<'PY'
 import json,sys
 try:

@@ -160,6 +160,36 @@ def test_f32_network_trains_on_the_streamed_kernels():
     assert loss1 < loss0
 
 
+def test_graphed_train_step_equals_eager():
+    """The captured step (forward, CE, backward, Adam in one CUDA graph) gives
+    the eager step's losses and parameters on the f32 streamed path (both run
+    the capturable Adam, whose bias corrections come from the device)."""
+    from paper_2501_14490_b200.net import Adam, GraphedTrainStep
+    z = _z()
+    x = torch.tensor(z["s0_x"], device="cuda", dtype=torch.float32)
+    y = torch.tensor(z["s0_y"], device="cuda")
+    nets, losses = [], []
+    for graphed in (False, True):
+        net = _net()
+        opt = Adam(net.parameters_list(), 1e-2)
+        opt.make_capturable()
+        if graphed:
+            step = GraphedTrainStep(net, opt, x, y, warmup=3)
+            ls = [float(step()[0]) for _ in range(3)]
+        else:
+            ls = []
+            for _ in range(6):
+                loss, _ = net.train_step_grads_async(x, y)
+                opt.step()
+                ls.append(float(loss))
+            ls = ls[3:]
+        nets.append(net)
+        losses.append(ls)
+    assert losses[0] == losses[1]
+    for a, b in zip(nets[0].parameters_list(), nets[1].parameters_list()):
+        assert torch.equal(a, b)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
