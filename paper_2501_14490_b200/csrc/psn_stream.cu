@@ -71,13 +71,15 @@ static unsigned long long wait_limit_ns() {
 bool eligible(const psn_desc_t* desc) {
   if (env_int("PSN_FORCE_GENERIC", 0)) return false;
   if (desc->dtype != PSN_F32 && desc->dtype != PSN_BF16) return false;
-  if (desc->Q != 1) return false;                 // spatial inputs: generic path
   if (desc->k > 8 || desc->d > 3) return false;   // instantiated orders / sawtooth dilations
+  // spatial inputs (Q > 1): the per-channel sums of a group are merged from its
+  // column sums in shared memory; the forward's 2 + 2k sums must fit the deposit
+  if (desc->Q > 1 && desc->k > 4) return false;
   if ((desc->k - 1) * desc->d > kMaxH) return false;
   if (desc->flags & PSN_SMOOTH) return false;     // SMOOTH (finite-difference checks): generic path
   const int es = (int)dtype_size(desc->dtype);
-  if ((desc->C * es) % 16 != 0) return false;     // TMA row stride must be a multiple of 16 B
-  if (desc->T > (1 << 30) || desc->N > (1 << 30) || desc->C > (1 << 30)) return false;
+  if ((desc->C * desc->Q * es) % 16 != 0) return false;  // TMA row stride must be a multiple of 16 B
+  if (desc->T > (1 << 30) || desc->N > (1 << 30) || desc->C > (1 << 30) || desc->Q > (1 << 20)) return false;
   return true;
 }
 
@@ -88,20 +90,38 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   const int g_sms = da->sms, g_smem_optin = da->smem_optin;
   const int es = (int)dtype_size(desc->dtype);
   if (desc->T > (1 << 24) || desc->C > (1 << 24)) return false;  // group / iteration indices stay small
-  if ((double)desc->T * desc->N * desc->C >= 4294967296.0) return false;  // 32-bit element offsets
+  if ((double)desc->T * desc->N * desc->C * desc->Q >= 4294967296.0) return false;  // 32-bit element offsets
   p.T = (int)desc->T;
   p.N = (int)desc->N;
   p.C = (int)desc->C;
-  p.J = p.C;
+  p.Q = (int)desc->Q;
+  p.J = p.C * p.Q;
+  // channel groups: whole channels, at most 32 (one fold lane each), their
+  // columns a multiple of 32 where the channel count allows (so no 32-column
+  // tile straddles two groups), and >= 256 columns when that is cheap
+  if (p.Q == 1) {
+    p.nch = kCols;
+  } else {
+    int g = p.Q, b = kCols;
+    while (b) {  // gcd(Q, 32)
+      const int t = g % b;
+      g = b;
+      b = t;
+    }
+    p.nch = kCols / g;
+    while (p.nch * 2 <= kCols && (long long)p.nch * p.Q < 256) p.nch *= 2;
+  }
+  if (p.nch > p.C) p.nch = p.C;
+  p.ncol = (int)(((long long)p.nch * p.Q + kCols - 1) / kCols);
   p.k = desc->k;
   p.d = desc->d;
   p.H = (p.k - 1) * p.d;
   const Layout L = layout_of(p.k, p.d, es, bwd);
   p.TB = L.TB;
-  p.G = (p.C + kCols - 1) / kCols;
+  p.G = (p.C + p.nch - 1) / p.nch;
   p.nbk = (p.N + kBoxN - 1) / kBoxN;
   p.ttl = (p.T + p.TB - 1) / p.TB;
-  const long long tpg = (long long)p.nbk * p.ttl;
+  const long long tpg = (long long)p.ncol * p.nbk * p.ttl;
   if (tpg * (long long)(g_sms + 1) >= (1LL << 32)) return false;  // 32-bit schedule arithmetic
   p.tpg = (int)tpg;
   p.nCTA = g_sms;

@@ -90,13 +90,15 @@ constexpr int kRowBlock = 4;                     // time rows a consumer thread 
 // plan + arguments (plain data, passed by value)
 // -------------------------------------------------------------------------
 struct Plan {
-  int T, N, J, C;  // J = C (Q == 1 on this path)
+  int T, N, J, C, Q;  // J = C * Q columns; channel(j) = j / Q
   int k, d, H;
   int TB;          // time rows per tile
-  int G;           // groups of 32 columns
-  int nbk;         // ceil(N / 8)
+  int G;           // groups of nch whole channels
+  int nch;         // channels per group (<= 32: one fold lane per channel)
+  int ncol;        // 32-column tiles per group = ceil(nch * Q / 32)
+  int nbk;         // ceil(N / kBoxN)
   int ttl;         // ceil(T / TB)
-  int tpg;         // tiles per group = nbk * ttl
+  int tpg;         // tiles per group = ncol * nbk * ttl (time fastest, then batch block, then column tile)
   int nCTA;
   int nT;          // CTA teams: team q = CTAs b with b % nT == q streams groups g with g % nT == q
   int lag;         // pass2 runs `lag` iterations behind pass1 (>= 1)
@@ -375,6 +377,18 @@ __device__ __forceinline__ void tile_range(const Plan& p, const Team& t, int v, 
 }
 
 
+// A group's tiles run time-fastest, then batch block, then 32-column tile:
+// stream block sb = tile / ttl is (column tile ct = sb / nbk, batch block nb).
+__device__ __forceinline__ void split_sb(const Plan& p, int sb, int& ct, int& nb) {
+  ct = (int)((unsigned)sb / (unsigned)p.nbk);
+  nb = sb - ct * p.nbk;
+}
+__device__ __forceinline__ int gcol0(const Plan& p, int g) { return g * p.nch * p.Q; }  // first column of group g
+__device__ __forceinline__ int gcolend(const Plan& p, int g) {
+  const long long e = (long long)(g + 1) * p.nch * p.Q;
+  return e < p.J ? (int)e : p.J;
+}
+
 enum ItemKind { kHead = 0, kTile = 1, kTail = 2 };
 
 // -------------------------------------------------------------------------
@@ -432,7 +446,7 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
   double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
   double* pd = (double*)prow;
   const int flags = a.flags;
-  const double m = (double)p.T * (double)p.N;
+  const double m = (double)p.T * (double)p.N * (double)p.Q;  // elements per channel
   if constexpr (!BWD) {
     const bool smooth = flags & PSN_SMOOTH;
     const bool use_batch = flags & PSN_USE_BATCH_STATS;
@@ -579,8 +593,8 @@ __device__ __forceinline__ void red_add_f64(double* a, double v) {
 __device__ __forceinline__ float ld_io(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float ld_io(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
 
-// Shift of the forward's pass-1 moments for column c: h1 of stream (n = 0, c)
-// at t = T - 1, computed like the consumers compute h1.  One sample of the
+// Shift of the forward's pass-1 moments for channel c: h1 of stream (n = 0,
+// first column of c) at t = T - 1, computed like the consumers compute h1.  One sample of the
 // channel's own distribution lies within a few standard deviations of its
 // mean, so the one-pass moments sum (h1 - shift) without the cancellation a
 // far-away shift (e.g. a stale running mean) would cause.  Every CTA derives
@@ -594,7 +608,7 @@ __device__ __forceinline__ double group_shift(const Args& a, const double* w, in
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const int t = ts - (K - 1 - i) * D;
-    const double xv = t >= 0 ? (double)ld_io(x + ((size_t)t * p.N) * p.J + c) : 0.0;
+    const double xv = t >= 0 ? (double)ld_io(x + ((size_t)t * p.N) * p.J + (size_t)c * p.Q) : 0.0;
     h = i == 0 ? w[0] * xv : fma(w[i], xv, h);
   }
   return round_f32_sg(h);
@@ -604,11 +618,13 @@ __device__ __forceinline__ double group_shift(const Args& a, const double* w, in
 // the kernel: warps 0..15 consume tiles, warp 16 issues TMA, warp 17
 // publishes the per-group sums, warp 18 folds (see the file header)
 // -------------------------------------------------------------------------
-template <int K, int D, typename IO, bool BWD>
+template <int K, int D, typename IO, bool BWD, bool SP>
 __global__ void __launch_bounds__(kThreads, 1)
     psn_stream_kernel(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxh,
                       const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
                       const Args a) {
+  // SP: spatial inputs (Q > 1, groups of several 32-column tiles); false: one
+  // column tile per group, lane = channel (the channel sums need no merge)
   using C_ = Cfg<K, D, IO, BWD>;
   constexpr Layout LY = C_::L;
   constexpr int H = C_::H, NV = C_::NV, TB = C_::TB;
@@ -634,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsumerWarps);
     }
-    mbar_init(depf, 8);  // the high warp of each consumer pair arrives
+    mbar_init(depf, kConsumerWarps);  // every consumer warp releases its deposit writes
     mbar_init(depe, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(p1f + i, 1);
@@ -647,6 +663,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   const Team tm = team_of(p);
+  auto sbsplit = [&](int sb, int& ct, int& nb) {
+    if constexpr (SP) {
+      split_sb(p, sb, ct, nb);
+    } else {
+      ct = 0;
+      nb = sb;
+    }
+  };
   const int iters = tm.ng > 0 ? tm.ng + p.lag : 0;
   auto gid = [&](int j) { return tm.q + j * p.nT; };  // team-local group index -> group
 
@@ -670,7 +694,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* st = smem + (size_t)s * C_::STAGE;
         uint64_t pol = (kind == kTile) ? (pass == 0 ? pol_keep : pol_drop) : (pass == 0 ? pol_keep : pol_norm);
         if (a.ablate & 64) pol = pol_norm;  // experiment: no L2 residency hints
-        const int c0 = g * kCols, n0 = nbi * kBoxN;
+        int ct, nb;
+        sbsplit(nbi, ct, nb);
+        const int c0 = gcol0(p, g) + ct * kCols, n0 = nb * kBoxN;
         if (a.ablate & 4) {
           mbar_arrive(full + s);
         } else if (kind == kTile) {
@@ -735,21 +761,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned long long tp_start = gtimer(), tp_dep = 0;
     int nd = 0;
     double nrm = 0.0, nrv = 0.0;
-    auto prefetch_stats = [&](int g) {
-      const int c = g * kCols + lane;
-      nrm = c < p.C ? __ldcg(a.rm + c) : 0.0;
-      nrv = c < p.C ? __ldcg(a.rv + c) : 0.0;
+    auto prefetch_stats = [&](int g) {  // lane = channel of the group
+      const int c = g * p.nch + lane;
+      const bool cv = lane < p.nch && c < p.C;
+      nrm = cv ? __ldcg(a.rm + c) : 0.0;
+      nrv = cv ? __ldcg(a.rv + c) : 0.0;
     };
     if (!BWD && tm.ng > 0) prefetch_stats(gid(0));
     // pass-1 parameters for local group j into slot j & 1 (freed by the
     // consumers' done_p1(j - 2))
     auto stage_p1 = [&](int j) {
       if (j >= 2) {
-        if (lane == 0) mbar_wait(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
+        mbar_wait(p1e + (j & 1), (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
         __syncwarp();
       }
-      const int c = gid(j) * kCols + lane;
-      const bool cv = c < p.C;
+      const int c = gid(j) * p.nch + lane;  // lane = channel of the group
+      const bool cv = lane < p.nch && c < p.C;
       const int cc = cv ? c : 0;
       double* d = (double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
       if constexpr (!BWD) {
@@ -773,7 +800,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tm.ng > 0) stage_p1(0);
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
       const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      if (lane == 0) mbar_wait(depf, (unsigned)(nd & 1), a.wait_ns);
+      mbar_wait(depf, (unsigned)(nd & 1), a.wait_ns);
       __syncwarp();
       if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
 #pragma unroll
@@ -849,9 +876,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < tm.ng; ++j) {
       const int g = gid(j);
       const int sl = j & 1;
-      const int c = g * kCols + lane;
+      const int c = g * p.nch + lane;  // lane = channel of the group
+      const bool cv = lane < p.nch && c < p.C;
       FoldIn<K, BWD> in;
-      if (c < p.C) load_fold_in<K, BWD>(a, c, in);
+      if (cv) load_fold_in<K, BWD>(a, c, in);
       unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
       if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)tm.sz, "pass-1 sums", a.wait_ns);
       __syncwarp();
@@ -861,10 +889,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         t0 = t1;
       }
       if (j >= 2) {
-        if (lane == 0) mbar_wait(p2e + sl, (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
+        mbar_wait(p2e + sl, (unsigned)(((j >> 1) - 1) & 1), a.wait_ns);
         __syncwarp();
       }
-      if (c < p.C) {
+      if (cv) {
         double tt[NV];
 #pragma unroll
         for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
@@ -925,42 +953,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
     mbar_wait(p2f + sl, (unsigned)((j >> 1) & 1), a.wait_ns);
     if (PSN_TRACE_BUILD && a.trace) tc_param += gtimer() - t0;
-    return p2s + sl * LY.pbytes + lane * LY.pstride;
+    return p2s + sl * LY.pbytes;  // the slot; channel chl's row at chl * pstride
   };
   auto done_params = [&](int j) {
     __syncwarp();
     if (lane == 0) mbar_arrive(p2e + (j & 1));
   };
-  // per-warp pass-1 sums handed to the publisher: warps w and w + 8 share slot w
-  // (the low warp stores, the high warp adds in fixed order and arrives)
-  auto deposit = [&](const double* acc, int nv) {
-    const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-    if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1), a.wait_ns);
-    if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
-    const int sw = warp & 7;
-    if (warp < 8) {
+  // Per-warp pass-1 sums handed to the publisher through the warp pair's
+  // channel-indexed slot (warps w and w + 8 share slot w).  A flush turns the
+  // lanes' column sums into channel sums: a channel's columns are a contiguous
+  // run of lanes (Q > 1), and an inclusive segmented scan in fixed order leaves
+  // the run's sum in its last lane (`tail`), which adds it at the channel's
+  // slot entry `chl`.  The low warp writes first (zeroing the slot at the
+  // range's first flush, once the publisher took the previous range's sums),
+  // then the high warp adds; end_deposit hands the slot over.
+  auto flush = [&](double* accv, int nv, int chl, int seg0, bool tail, bool first) {
+    if (first) {
+      const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
+      if (nd >= 1) mbar_wait(depe, (unsigned)((nd - 1) & 1), a.wait_ns);
+      if (PSN_TRACE_BUILD && a.trace) tc_dep += gtimer() - t0;
+    }
+    if constexpr (SP) {
 #pragma unroll
-      for (int val = 0; val < kMaxNV; ++val)
-        if (val < nv) dep[(sw * kMaxNV + val) * kCols + lane] = acc[val];
+      for (int val = 0; val < kMaxNV; ++val) {
+        if (val < nv) {
+          double v = accv[val];
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double u = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane - off >= seg0) v += u;
+          }
+          accv[val] = v;
+        }
+      }
+    }
+    const int sw = warp & 7;
+    double* slot = dep + sw * kMaxNV * kCols;
+    if (warp < 8) {
+      if (first) {
+#pragma unroll
+        for (int val = 0; val < kMaxNV; ++val)
+          if (val < nv) slot[val * kCols + lane] = 0.0;
+        __syncwarp();
+      }
+      if (tail) {
+#pragma unroll
+        for (int val = 0; val < kMaxNV; ++val)
+          if (val < nv) slot[val * kCols + chl] += accv[val];
+      }
     }
     asm volatile("bar.sync %0, 64;" ::"r"(2 + sw) : "memory");  // pair barrier (warps sw, sw + 8)
-    if (warp >= 8) {
+    if (warp >= 8 && tail) {
 #pragma unroll
       for (int val = 0; val < kMaxNV; ++val)
-        if (val < nv) dep[(sw * kMaxNV + val) * kCols + lane] += acc[val];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(depf);
+        if (val < nv) slot[val * kCols + chl] += accv[val];
     }
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + sw) : "memory");
+#pragma unroll
+    for (int val = 0; val < kMaxNV; ++val)
+      if (val < nv) accv[val] = 0.0;
+  };
+  auto end_deposit = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(depf);
     ++nd;
+  };
+  // column -> (its channel's slot in the group, first lane of the channel's run
+  // in this 32-column tile, whether this lane ends the run)
+  struct ColInfo {
+    int col, chl, seg0;
+    bool valid, tail;
+  };
+  auto col_info = [&](int g, int ct) {
+    ColInfo ci;
+    const int gc0 = gcol0(p, g), gce = gcolend(p, g);
+    ci.col = gc0 + ct * kCols + lane;
+    ci.valid = ci.col < gce;
+    const int cq = ci.valid ? (int)((unsigned)ci.col / (unsigned)p.Q) : g * p.nch;
+    ci.chl = cq - g * p.nch;
+    const int inq = ci.valid ? ci.col - cq * p.Q : 0;
+    ci.seg0 = lane - (lane < inq ? lane : inq);
+    ci.tail = ci.valid && (lane == kCols - 1 || ci.col + 1 >= gce || inq == p.Q - 1);
+    return ci;
   };
   const size_t rowstride = (size_t)p.N * p.J;
   const uint32_t rs32 = (uint32_t)rowstride;  // the planner guarantees T*N*C < 2^32
   const unsigned mN = (unsigned)p.N;
   // pass-1 parameters of local group j (W and the moment shift, or the
   // forward's w_q and b_f): staged in shared memory by the publisher warp
-  auto take_p1 = [&](int j) -> const double* {
+  auto take_p1 = [&](int j) -> const double* {  // the slot; channel chl's row at chl * (K + 1)
     mbar_wait(p1f + (j & 1), (unsigned)((j >> 1) & 1), a.wait_ns);
-    return (const double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
+    return (const double*)(p1s + (j & 1) * LY.pbytes);
   };
   auto done_p1 = [&](int j) {
     __syncwarp();
@@ -976,29 +1059,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int g = gid(it);
       const int v = worker_of(tm, it, 0);
-      const int col = g * kCols + lane;
       int t_a, t_b;
       tile_range(p, tm, v, t_a, t_b);
       if (v >= tm.P) t_a = t_b = 0;
       double acc[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) acc[u] = 0.0;
+      const double* p1b = take_p1(it);
+      int cur_ct = -1;  // the 32-column tile the lane's parameters / sums belong to
+      bool first_flush = true;
+      ColInfo ci{};
       if constexpr (!BWD) {
         // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
         constexpr int U = PSN_U_F1;
-        double w[K], xw[H + U], sh, sxa = 0.0;
-        {
-          const double* pp = take_p1(it);
-          for (int i = 0; i < K; ++i) w[i] = ldsd(pp + i);
-          sh = ldsd(pp + K);
-          done_p1(it);
-        }
+        double w[K], xw[H + U], sh = 0.0, sxa = 0.0;
+        auto flush_f = [&]() {  // column sums -> channel sums (sxa: sum of x over the rows)
+#pragma unroll
+          for (int i = 0; i < K; ++i) acc[2 + K + i] += sxa;
+          sxa = 0.0;
+          const ColInfo cf = SP ? ci : col_info(g, 0);  // (non-spatial: recomputed, not kept live)
+          flush(acc, NV, cf.chl, cf.seg0, cf.tail, first_flush);
+          first_flush = false;
+        };
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        int ct, nb;
+        sbsplit(nbi, ct, nb);
         opaque(nbi);
         opaque(tt);
+        auto params_f = [&]() {
+          const double* pp = p1b + ci.chl * (K + 1);
+#pragma unroll
+          for (int i = 0; i < K; ++i) w[i] = ldsd(pp + i);
+          sh = ldsd(pp + K);
+        };
+        if constexpr (!SP) {
+          ci = col_info(g, 0);
+          params_f();
+        }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
-          const bool lv = (unsigned)(nbi * kBoxN + n_in) < mN && col < p.J;
+          if constexpr (SP) {
+            if (ct != cur_ct) {
+              if (tile != t_a) flush_f();
+              ci = col_info(g, ct);
+              cur_ct = ct;
+              params_f();
+            }
+          }
+          const int col = ci.col;
+          const bool lv = (unsigned)(nb * kBoxN + n_in) < mN && ci.valid;
           if (tile == t_a || tt == 0) {
 #pragma unroll
             for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
@@ -1059,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // end of the stream: Sx_i = sum_{t < T - off_i} x[t] drops the last off_i
             // samples of the stream (loaded from global: H values once per stream)
             if (tt == p.ttl - 1 && lv) {
-              const IO* xp = (const IO*)a.x + (size_t)(nbi * kBoxN + n_in) * p.J + col;
+              const IO* xp = (const IO*)a.x + (size_t)(nb * kBoxN + n_in) * p.J + col;
 #pragma unroll
               for (int r = 0; r < H; ++r) {
                 const int t = p.T - 1 - r;
@@ -1073,12 +1182,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
+            sbsplit(nbi, ct, nb);
           }
           opaque(tt);
           opaque(nbi);
         }
-#pragma unroll
-        for (int i = 0; i < K; ++i) acc[2 + K + i] += sxa;  // sxa: sum of x over this thread's rows
+        if (t_b > t_a) flush_f();
       } else {
         // ---- backward pass 1: db, dw_q -- f64 end to end (h2 exact and f32-rounded like the
         // reference's carrier, sigma' and dh2 in f64): f32 per-element errors (~1e-7) would
@@ -1086,22 +1195,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         // entries.  (The BN term of dW comes from the forward's data sums.)  Rows
         // alternate between two f64 accumulator sets (ILP).
         constexpr int U = PSN_U_B1;
-        double wq[K], xd[H + U], acc2[1 + K];
+        double wq[K], xd[H + U], acc2[1 + K], bf = 0.0;
 #pragma unroll
         for (int i = 0; i <= K; ++i) acc2[i] = 0.0;
+        auto flush_b = [&]() {  // column sums -> channel sums
 #pragma unroll
-        double bf;
-        {
-          const double* pp = take_p1(it);
+          for (int i = 0; i <= K; ++i) {
+            acc[i] += acc2[i];
+            acc2[i] = 0.0;
+          }
+          const ColInfo cf = SP ? ci : col_info(g, 0);
+          flush(acc, NV, cf.chl, cf.seg0, cf.tail, first_flush);
+          first_flush = false;
+        };
+        const double scc = a.scc;
+        int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        int ct, nb;
+        sbsplit(nbi, ct, nb);
+        opaque(nbi);
+        opaque(tt);
+        auto params_b = [&]() {
+          const double* pp = p1b + ci.chl * (K + 1);
+#pragma unroll
           for (int i = 0; i < K; ++i) wq[i] = ldsd(pp + i);
           bf = ldsd(pp + K);
-          done_p1(it);
+        };
+        if constexpr (!SP) {
+          ci = col_info(g, 0);
+          params_b();
         }
-        const double scc = a.scc;
-        int tt = t_a % p.ttl;
-        opaque(tt);
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          if constexpr (SP) {
+            if (ct != cur_ct) {
+              if (tile != t_a) flush_b();
+              ci = col_info(g, ct);
+              cur_ct = ct;
+              params_b();
+            }
+          }
           if (tile == t_a || tt == 0) {
 #pragma unroll
             for (int j = 0; j < H + U; ++j) xd[j] = 0.0;
@@ -1153,13 +1285,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           };
           if (!(a.ablate & 1)) rows();
           release_item();
-          if (++tt == p.ttl) tt = 0;
+          if (++tt == p.ttl) {
+            tt = 0;
+            ++nbi;
+            sbsplit(nbi, ct, nb);
+          }
           opaque(tt);
+          opaque(nbi);
         }
-#pragma unroll
-        for (int i = 0; i <= K; ++i) acc[i] += acc2[i];
+        if (t_b > t_a) flush_b();
       }
-      if (v < tm.P) deposit(acc, NV);  // CTA reduction + publication happen on the publisher warp
+      done_p1(it);
+      if (v < tm.P) end_deposit();  // CTA reduction + publication happen on the publisher warp
       if (PSN_TRACE_BUILD && a.trace) tc_pass[0] += gtimer() - tc_t;
     }
     // ------------------------------------------------------------- pass 2
@@ -1171,8 +1308,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j = it - p.lag;
       const int g = gid(j);
       const int v = worker_of(tm, j, 1);
-      const unsigned char* pr = take_params(j);
-      const int col = g * kCols + lane;
+      const unsigned char* p2b = take_params(j);
+      int cur_ct = -1;
+      ColInfo ci{};
       int t_a, t_b;
       tile_range(p, tm, v, t_a, t_b);
       if (v >= tm.P) t_a = t_b = 0;
@@ -1180,19 +1318,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!BWD) {
         // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
         constexpr int U = PSN_U_F2;
-        double wq[K], xw[H + U];
-        const double* pd = (const double*)pr;
-#pragma unroll
-        for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
-        const double bf = ldsd(pd + K);
-        done_params(j);
+        double wq[K], xw[H + U], bf = 0.0;
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        int ct, nb;
+        sbsplit(nbi, ct, nb);
         opaque(nbi);
         opaque(tt);
+        auto params_f2 = [&]() {  // the lane's channel parameters for this column tile
+          const double* pd = (const double*)(p2b + ci.chl * LY.pstride);
+#pragma unroll
+          for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
+          bf = ldsd(pd + K);
+        };
+        if constexpr (!SP) {
+          ci = col_info(g, 0);
+          params_f2();
+        }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
-          const int n = nbi * kBoxN + n_in;
-          const bool lv = (unsigned)n < mN && col < p.J;
+          if constexpr (SP) {
+            if (ct != cur_ct) {
+              ci = col_info(g, ct);
+              cur_ct = ct;
+              params_f2();
+            }
+          }
+          const int col = ci.col;
+          const int n = nb * kBoxN + n_in;
+          const bool lv = (unsigned)n < mN && ci.valid;
           if (tile == t_a || tt == 0) {
 #pragma unroll
             for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
@@ -1237,10 +1390,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
+            sbsplit(nbi, ct, nb);
           }
           opaque(tt);
           opaque(nbi);
         }
+        done_params(j);
       } else {
         // ---- backward pass 2: dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i]
         // (time-reversed conv as a scatter into an (H+U)-slot ring: slot j holds the
@@ -1248,24 +1403,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         // are complete).  The BN term of dW comes from the forward's exact data
         // sums (fold_channel), so this pass only writes dx.
         constexpr int U = PSN_U_B2;
-        float w[K], wq[K], xw[H + U], pacc[H + U];
-        const double* pd = (const double*)pr;
-        const float* pf = (const float*)(pr + 8 * (K + 1));
+        float w[K], wq[K], wqs[K], xw[H + U], pacc[H + U];
         // surrogate.py: sigma'(h) = scale / (1 + cc h^2), cc = (pi alpha / 2)^2 (arctan) or
         // alpha (rational); the scale is folded into the w_q taps of the scatter
         const float cc = a.sur.kind == PSN_ARCTAN ? a.sur.c * a.sur.c : a.sur.c;
+        float bf = 0.f, mu = 0.f, a1 = 0.f, b1 = 0.f, cx = 0.f;
+        auto load_params = [&]() {  // the lane's channel parameters (fold_channel) for this column tile
+          const unsigned char* pr = p2b + ci.chl * LY.pstride;
+          const double* pd = (const double*)pr;
+          const float* pf = (const float*)(pr + 8 * (K + 1));
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          wq[i] = (float)ldsd(pd + i);
-          w[i] = ldsf(pf + i);
-        }
-        const float bf = (float)ldsd(pd + K);  // b_f + c sum w_q   (centred inputs, fold_channel)
-        const float mu = ldsf(pf + K), a1 = ldsf(pf + K + 1), b1 = ldsf(pf + K + 2);  // mu - c sum W
-        const float cx = ldsf(pf + K + 3);
-        float wqs[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) wqs[i] = wq[i] * a.sur.scale;
-        done_params(j);
+          for (int i = 0; i < K; ++i) {
+            wq[i] = (float)ldsd(pd + i);
+            w[i] = ldsf(pf + i);
+            wqs[i] = wq[i] * a.sur.scale;
+          }
+          bf = (float)ldsd(pd + K);  // b_f + c sum w_q   (centred inputs)
+          mu = ldsf(pf + K);         // mu - c sum W
+          a1 = ldsf(pf + K + 1);
+          b1 = ldsf(pf + K + 2);
+          cx = ldsf(pf + K + 3);
+        };
         int run_t0 = 0;
         bool lv = false;
         uint32_t obase = 0;
@@ -1314,14 +1472,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
+        int ct, nb;
+        sbsplit(nbi, ct, nb);
         opaque(nbi);
         opaque(tt);
+        if constexpr (!SP) {
+          ci = col_info(g, 0);
+          load_params();
+        }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          if constexpr (SP) {
+            if (ct != cur_ct) {
+              ci = col_info(g, ct);
+              cur_ct = ct;
+              load_params();
+            }
+          }
           if (tile == t_a || tt == 0) {
-            const int n = nbi * kBoxN + n_in;
-            lv = (unsigned)n < mN && col < p.J;
-            obase = (uint32_t)(lv ? n : 0) * (uint32_t)p.J + (uint32_t)(lv ? col : 0);
+            const int n = nb * kBoxN + n_in;
+            lv = (unsigned)n < mN && ci.valid;
+            obase = (uint32_t)(lv ? n : 0) * (uint32_t)p.J + (uint32_t)(lv ? ci.col : 0);
             run_t0 = t0;
 #pragma unroll
             for (int j = 0; j < H + U; ++j) {
@@ -1398,10 +1569,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++tt == p.ttl) {
             tt = 0;
             ++nbi;
+            sbsplit(nbi, ct, nb);
           }
           opaque(tt);
           opaque(nbi);
         }
+        done_params(j);
       }
       if (PSN_TRACE_BUILD && a.trace) tc_pass[1] += gtimer() - tc_t;
     }
@@ -1421,14 +1594,14 @@ int stream_encode_maps(const Plan& p, int es, bool bwd, const void* x, const voi
 // device / context (occupancy, MPS or partition limits) -- run the generic path
 constexpr int kFallback = -1;
 
-template <int K, int D, typename IO, bool BWD>
+template <int K, int D, typename IO, bool BWD, bool SP>
 int stream_launch(const Args& args, const void* x, const void* dy, cudaStream_t st) {
   using C_ = Cfg<K, D, IO, BWD>;
   CUtensorMap maps[4];
   int rc = stream_encode_maps(args.p, (int)sizeof(IO), BWD, x, dy, maps);
   if (rc) return rc;
   const size_t smem = (size_t)args.p.S * C_::STAGE + C_::L.fixed + 16 * (size_t)args.p.S + 1024;
-  auto kern = psn_stream_kernel<K, D, IO, BWD>;
+  auto kern = psn_stream_kernel<K, D, IO, BWD, SP>;
   cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (stream kernel smem) failed");
   int occ = 0;

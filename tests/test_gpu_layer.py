@@ -122,7 +122,11 @@ def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0, s
     p.W = layer.W.detach().cpu().numpy()[sel]
     ref_out, cache, dx, dW, dg, db = O.train_step(p, xs, dys)
     st = {kk: v.cpu().numpy()[sel] for kk, v in layer.last_state().items()}
-    assert_rel(st["mu"], cache.mu, 1e-10, "mu")
+    # mean: 1e-10 relative, or 1e-12 of the channel's spread when the mean is
+    # near zero (any two summation orders of the reference's mean differ by
+    # ~1e-16 * mean|h1|, so a relative bound alone is ill-conditioned there)
+    mu_err = np.abs(st["mu"] - cache.mu)
+    assert np.all(mu_err <= 1e-10 * np.abs(cache.mu) + 1e-12 * cache.s), f"mu: max err {mu_err.max():.3e}"
     assert_rel(st["a"], cache.a, 1e-12, "a")
     assert np.array_equal(st["w_q"], cache.w_q)
     got = out.detach().float().cpu().numpy()[:, :, sel]
@@ -187,6 +191,25 @@ def test_dvs_lip_shape_bf16_parity():
     I/O (BASELINE configs[3]); oracle on the bf16 inputs widened to f32."""
     _oracle_subset_check(30, 32, 64, 2, 2, channels=[0, 31, 63], dtype=torch.bfloat16, seed=30,
                          spatial=(22, 22))
+
+
+@pytest.mark.parametrize("shape,k,d,dt", [
+    ((64, 20, 40, 3, 3), 4, 3, torch.float32),    # Q = 9: 32 channels per group, 9 column tiles
+    ((40, 16, 13, 12), 3, 2, torch.float32),      # Q = 12, C = 13: one partial group
+    ((48, 18, 40, 12), 2, 1, torch.float32),      # Q = 12, C = 40: 2 groups, the last partial
+    ((32, 24, 48, 32), 4, 1, torch.float32),      # Q = 32 (seq-CIFAR conv stage): 8 channels per group
+    ((30, 32, 16, 22, 22), 2, 3, torch.bfloat16), # Q = 484 (DVS-Lip stage 1), bf16
+])
+def test_spatial_inputs_streamed_parity(shape, k, d, dt):
+    """Spatial inputs [T, N, C, H(, W)] on the streamed kernels: channel groups
+    span several 32-column tiles and the per-channel sums merge the column sums
+    (segmented warp scan); every channel against the oracle."""
+    from paper_2501_14490_b200 import _lib as L
+    desc = L.make_desc(shape, k, d, dt, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+    assert L.plan_info(desc, False)["streamed"] == 1 and L.plan_info(desc, True)["streamed"] == 1
+    T, N, C = shape[:3]
+    _oracle_subset_check(T, N, C, k, d, channels=list(range(C)), dtype=dt, seed=sum(shape) + k,
+                         spatial=shape[3:])
 
 
 def test_bitwise_reproducible_run_to_run():
