@@ -236,9 +236,9 @@ __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target,
   if (ld_acquire(a) >= target) return;
   const unsigned long long t0 = gtimer();
   unsigned v;
-  while ((v = ld_acquire(a)) < target) {
-    __nanosleep(1000);
-    if (lim && gtimer() - t0 > lim) expired(what, (int)v, (int)target);
+  for (unsigned n = 1; (v = ld_acquire(a)) < target; ++n) {
+    __nanosleep(128);  // short: this wait is on the critical path of every group's fold
+    if ((n & 255u) == 0 && lim && gtimer() - t0 > lim) expired(what, (int)v, (int)target);
   }
 }
 
@@ -317,7 +317,7 @@ __host__ __device__ constexpr Layout layout_of(int k, int d, int es, bool bwd) {
   L.dbytes = bwd ? xrows * L.rowb : 0;
   // per-lane parameters: fwd f64 {W or w_q}[k] + {shift or b_f}; bwd f64 w_q[k], b_f + f32 W[k], mu, a1, b1, c
   // per-lane pass-2 parameters: fwd f64 w_q[k], b_f; bwd f64 w_q[k], b_f' + f32 W[k], mu', a1, b1, c
-  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 4) + 15) / 16 * 16 : 8 * (k + 1);
+  L.pstride = bwd ? (8 * (k + 1) + 4 * (k + 4) + 15) / 16 * 16 : 8 * (k + 2);
   L.pbytes = (kCols * L.pstride + 127) / 128 * 128;
   L.stage = (L.xbytes + L.dbytes + 1023) / 1024 * 1024;
   L.dep = 8 * L.NV * kCols * 8;  // per-warp-pair partial sums handed to the publisher
@@ -440,7 +440,7 @@ __device__ __forceinline__ void load_fold_in(const Args& a, int c, FoldIn<K, BWD
 // -------------------------------------------------------------------------
 template <int K, bool BWD>
 __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<K, BWD>& in, const double* tt,
-                                             double rm_prev, double rv_prev, double sh, bool store,
+                                             double rm_prev, double rv_prev, double sh, double cxs, bool store,
                                              unsigned char* prow) {
   const Plan& p = a.p;
   double* fr = a.fold + (size_t)c * PSN_FOLD_STRIDE(K);
@@ -477,14 +477,16 @@ __device__ __forceinline__ void fold_channel(const Args& a, int c, const FoldIn<
       fr[4] = mu_b;
       fr[5] = var_b;
       fr[6] = 1.0;  // BN-term data sums present
-      // data terms of the BN-through-statistics dW (network.py:298-315), exact in
-      // f64: Sx_i = sum x[t-off_i], Cx_i = sum x[t-off_i] (h1[t] - mu_b); pass 1
-      // summed P_i = sum x[t-off_i] (h1[t] - shift)
+      // data terms of the BN-through-statistics dW (network.py:298-315):
+      // Sx_i = sum x[t-off_i] and Cx_i = sum x[t-off_i] (h1[t] - mu_b).  Pass 1
+      // summed the centred D_i = sum (x[t-off_i] - cx) (x = 0 before the stream
+      // start) and P_i = sum (x[t-off_i] - cx)(h1[t] - shift); since
+      // sum_t (h1[t] - mu_b) = 0, Cx_i = P_i - (mu_b - shift) D_i exactly.
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        const double sx = tt[2 + K + i];
-        fr[PSN_FOLD_HDR + 2 * K + i] = sx;
-        fr[PSN_FOLD_HDR + 3 * K + i] = tt[2 + i] - (mu_b - sh) * sx;
+        const double di = tt[2 + K + i];
+        fr[PSN_FOLD_HDR + 2 * K + i] = di + cxs * m;
+        fr[PSN_FOLD_HDR + 3 * K + i] = tt[2 + i] - (mu_b - sh) * di;
       }
     }
 #pragma unroll
@@ -599,18 +601,21 @@ __device__ __forceinline__ float ld_io(const __nv_bfloat16* p) { return __bfloat
 // mean, so the one-pass moments sum (h1 - shift) without the cancellation a
 // far-away shift (e.g. a stale running mean) would cause.  Every CTA derives
 // the same value from the same data.
+// The same stream's newest sample x[T - 1] is the centring value `cx` of the
+// forward's f32 BN-term data sums (pass 1).
 template <int K, int D, typename IO>
-__device__ __forceinline__ double group_shift(const Args& a, const double* w, int c) {
+__device__ __forceinline__ double group_shift(const Args& a, const double* w, int c, double& cx) {
   const Plan& p = a.p;
   const IO* x = (const IO*)a.x;
   const int ts = p.T - 1;
-  double h = 0.0;
+  double h = 0.0, xv = 0.0;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const int t = ts - (K - 1 - i) * D;
-    const double xv = t >= 0 ? (double)ld_io(x + ((size_t)t * p.N) * p.J + (size_t)c * p.Q) : 0.0;
+    xv = t >= 0 ? (double)ld_io(x + ((size_t)t * p.N) * p.J + (size_t)c * p.Q) : 0.0;
     h = i == 0 ? w[0] * xv : fma(w[i], xv, h);
   }
+  cx = xv;
   return round_f32_sg(h);
 }
 
@@ -778,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = gid(j) * p.nch + lane;  // lane = channel of the group
       const bool cv = lane < p.nch && c < p.C;
       const int cc = cv ? c : 0;
-      double* d = (double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 1);
+      double* d = (double*)(p1s + (j & 1) * LY.pbytes) + lane * (K + 2);
       if constexpr (!BWD) {
         const double* Wc = a.W + (size_t)(a.shared ? 0 : cc) * K;
         double wl[K];
@@ -787,7 +792,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           wl[i] = cv ? __ldg(Wc + i) : 0.0;
           d[i] = wl[i];
         }
-        d[K] = cv ? group_shift<K, D, IO>(a, wl, cc) : 0.0;  // shift of the pass-1 moments
+        double cxs = 0.0;
+        d[K] = cv ? group_shift<K, D, IO>(a, wl, cc, cxs) : 0.0;  // shift of the pass-1 moments
+        d[K + 1] = cxs;                                           // centring of the BN-term data sums
       } else {
         const double* f = a.fold + (size_t)cc * PSN_FOLD_STRIDE(K);
 #pragma unroll
@@ -879,7 +886,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = g * p.nch + lane;  // lane = channel of the group
       const bool cv = lane < p.nch && c < p.C;
       FoldIn<K, BWD> in;
-      if (cv) load_fold_in<K, BWD>(a, c, in);
+      double sh = 0.0, cxs = 0.0;  // static fold inputs: loaded before the wait hides their latency
+      if (cv) {
+        load_fold_in<K, BWD>(a, c, in);
+        if constexpr (!BWD) sh = group_shift<K, D, IO>(a, in.W, c, cxs);
+      }
       unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
       if (lane == 0 && !(a.ablate & 2)) wait_counter(a.cnt + g, (unsigned)tm.sz, "pass-1 sums", a.wait_ns);
       __syncwarp();
@@ -898,9 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int val = 0; val < NV; ++val) tt[val] = __ldcg(a.acc + ((size_t)g * NV + val) * kCols + lane);
         const double rmp = BWD ? 0.0 : prev[((j & 7) * 2 + 0) * kCols + lane];
         const double rvp = BWD ? 0.0 : prev[((j & 7) * 2 + 1) * kCols + lane];
-        double sh = 0.0;
-        if constexpr (!BWD) sh = group_shift<K, D, IO>(a, in.W, c);
-        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, sh, designated(tm, j),
+        fold_channel<K, BWD>(a, c, in, tt, rmp, rvp, sh, cxs, designated(tm, j),
                              p2s + sl * LY.pbytes + lane * LY.pstride);
       } else {
         double* pd = (double*)(p2s + sl * LY.pbytes + lane * LY.pstride);
@@ -1041,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const unsigned mN = (unsigned)p.N;
   // pass-1 parameters of local group j (W and the moment shift, or the
   // forward's w_q and b_f): staged in shared memory by the publisher warp
-  auto take_p1 = [&](int j) -> const double* {  // the slot; channel chl's row at chl * (K + 1)
+  auto take_p1 = [&](int j) -> const double* {  // the slot; channel chl's row at chl * (K + 2)
     mbar_wait(p1f + (j & 1), (unsigned)((j >> 1) & 1), a.wait_ns);
     return (const double*)(p1s + (j & 1) * LY.pbytes);
   };
@@ -1070,13 +1079,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool first_flush = true;
       ColInfo ci{};
       if constexpr (!BWD) {
-        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps)
+        // ---- forward pass 1: shifted moments of h1 = f32(sum_i W_i x[t-off_i]) (f64 taps, f64
+        // moments) and the BN-term data sums of the backward's dW on the FP32 pipe (the FP64
+        // pipe bounds this pass): P_i = sum (x[t-off_i] - cx)(h1[t] - shift) and
+        // D_i = sum (x[t-off_i] - cx), centred by a sample cx of the channel so the f32
+        // products carry no common offset; f32 over 16 rows, f64 beyond (fold_channel)
         constexpr int U = PSN_U_F1;
-        double w[K], xw[H + U], sh = 0.0, sxa = 0.0;
-        auto flush_f = [&]() {  // column sums -> channel sums (sxa: sum of x over the rows)
+        constexpr int FR = 16;  // rows per f32 partial of the data sums
+        double w[K], xw[H + U], sh = 0.0;
+        float xt[H + U], pf[K], sxf = 0.f, shf = 0.f, cxf = 0.f;
 #pragma unroll
-          for (int i = 0; i < K; ++i) acc[2 + K + i] += sxa;
-          sxa = 0.0;
+        for (int i = 0; i < K; ++i) pf[i] = 0.f;
+        auto flush_f = [&]() {  // column sums -> channel sums
           const ColInfo cf = SP ? ci : col_info(g, 0);  // (non-spatial: recomputed, not kept live)
           flush(acc, NV, cf.chl, cf.seg0, cf.tail, first_flush);
           first_flush = false;
@@ -1087,10 +1101,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         opaque(nbi);
         opaque(tt);
         auto params_f = [&]() {
-          const double* pp = p1b + ci.chl * (K + 1);
+          const double* pp = p1b + ci.chl * (K + 2);
 #pragma unroll
           for (int i = 0; i < K; ++i) w[i] = ldsd(pp + i);
           sh = ldsd(pp + K);
+          shf = (float)sh;  // exact: the shift is an f32-rounded membrane
+          cxf = (float)ldsd(pp + K + 1);  // exact: a sample of x
         };
         if constexpr (!SP) {
           ci = col_info(g, 0);
@@ -1110,13 +1126,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)(nb * kBoxN + n_in) < mN && ci.valid;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+            for (int j = 0; j < H + U; ++j) {
+              xw[j] = 0.0;
+              xt[j] = -cxf;  // before the stream start: x = 0
+            }
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
+            for (int r = 0; r < H; ++r) {
+              const float xv = ldsx<IO>(xs + (r) * RSB);
+              xw[r] = (double)xv;
+              xt[r] = xv - cxf;
+            }
             release_item();
           }
           const uint32_t st = wait_item();
@@ -1131,7 +1154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + (r0 + u) * RSB);
+              for (int u = 0; u < U; ++u) {
+                const float xv = ldsx<IO>(xs + (r0 + u) * RSB);
+                xw[H + u] = (double)xv;
+                xt[H + u] = xv - cxf;
+              }
               double h[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) h[u] = w[0] * xw[u + slot<K, D>(0)];
@@ -1141,18 +1168,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u) h[u] = fma(w[i], xw[u + slot<K, D>(i)], h[u]);
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                double hc = round_f32_sg(h[u]) - sh;
-                if (!FULL && !(r0 + u < nvalid)) hc = 0.0;
+                const float hr32 = __double2float_rn(h[u]);  // the reference's f32 membrane (F2F, XU pipe)
+                const bool ok = FULL || r0 + u < nvalid;
+                const double hc = ok ? (double)hr32 - sh : 0.0;
+                const float hcf = ok ? hr32 - shf : 0.f;
                 S1[u] += hc;
                 S2[u] = fma(hc, hc, S2[u]);
-                // BN-term data sums of the backward's dW: P_i += x[t-off_i] (h1[t] - shift)
-                // (exact products, f64 sums; padding lanes and rows >= T see x = 0 / hc = 0)
 #pragma unroll
-                for (int i = 0; i < K; ++i) acc[2 + i] = fma(xw[u + slot<K, D>(i)], hc, acc[2 + i]);
-                sxa += xw[H + u];
+                for (int i = 0; i < K; ++i) pf[i] = fmaf(xt[u + slot<K, D>(i)], hcf, pf[i]);
+                sxf += ok ? xt[H + u] : 0.f;
+              }
+              if ((r0 + U) % FR == 0 || r0 + U == TB) {  // f32 partials -> f64 (padding lanes dropped)
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  if (lv) acc[2 + i] += (double)pf[i];
+                  pf[i] = 0.f;
+                }
+                if (lv) {
+#pragma unroll
+                  for (int i = 0; i < K; ++i) acc[2 + K + i] += (double)sxf;
+                }
+                sxf = 0.f;
               }
 #pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+              for (int j = 0; j < H; ++j) {
+                xw[j] = xw[j + U];
+                xt[j] = xt[j + U];
+              }
             }
           };
           if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
@@ -1165,8 +1207,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           release_item();
           if constexpr (H > 0) {
-            // end of the stream: Sx_i = sum_{t < T - off_i} x[t] drops the last off_i
-            // samples of the stream (loaded from global: H values once per stream)
+            // end of the stream: D_i = sum_{t < T} (x[t] - cx) - sum_{t >= T - off_i} x[t]
+            // (the cx of the last off_i samples and of the off_i window samples before
+            // the stream start cancel); the tail is loaded from global, H values per stream
             if (tt == p.ttl - 1 && lv) {
               const IO* xp = (const IO*)a.x + (size_t)(nb * kBoxN + n_in) * p.J + col;
 #pragma unroll
@@ -1215,7 +1258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         opaque(nbi);
         opaque(tt);
         auto params_b = [&]() {
-          const double* pp = p1b + ci.chl * (K + 1);
+          const double* pp = p1b + ci.chl * (K + 2);
 #pragma unroll
           for (int i = 0; i < K; ++i) wq[i] = ldsd(pp + i);
           bf = ldsd(pp + K);
