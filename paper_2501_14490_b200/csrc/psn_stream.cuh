@@ -655,13 +655,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsumerWarps);
     }
-    mbar_init(depf, kConsumerWarps);  // every consumer warp releases its deposit writes
-    mbar_init(depe, 1);
+    // shared-memory hand-offs between warps (deposits, parameter slots): every
+    // thread arrives, so each one releases its own accesses (a per-thread
+    // release-acquire pair per access, as compute-sanitizer racecheck models it)
+    mbar_init(depf, kConsumerWarps * 32);
+    mbar_init(depe, 32);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(p1f + i, 1);
-      mbar_init(p1e + i, kConsumerWarps);
-      mbar_init(p2f + i, 1);
-      mbar_init(p2e + i, kConsumerWarps);
+      mbar_init(p1f + i, 32);
+      mbar_init(p1e + i, kConsumerWarps * 32);
+      mbar_init(p2f + i, 32);
+      mbar_init(p2e + i, kConsumerWarps * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -802,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         d[K] = cv ? __ldg(f + 3) : 0.0;                                                // b_f
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(p1f + (j & 1));
+      mbar_arrive(p1f + (j & 1));
     };
     if (tm.ng > 0) stage_p1(0);
     auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
@@ -820,7 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(depe);
+      mbar_arrive(depe);
       ++nd;
     };
     for (int it = 0; it < iters; ++it) {
@@ -917,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < LY.pstride / 8; ++i) pd[i] = 0.0;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(p2f + sl);
+      mbar_arrive(p2f + sl);
       if (PSN_TRACE_BUILD && a.trace) tf_fold += gtimer() - t0;
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
@@ -966,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   auto done_params = [&](int j) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(p2e + (j & 1));
+    mbar_arrive(p2e + (j & 1));
   };
   // Per-warp pass-1 sums handed to the publisher through the warp pair's
   // channel-indexed slot (warps w and w + 8 share slot w).  A flush turns the
@@ -1024,7 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   auto end_deposit = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(depf);
+    mbar_arrive(depf);
     ++nd;
   };
   // column -> (its channel's slot in the group, first lane of the channel's run
@@ -1056,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   auto done_p1 = [&](int j) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(p1e + (j & 1));
+    mbar_arrive(p1e + (j & 1));
   };
 
   for (int it = 0; it < iters; ++it) {
