@@ -1572,11 +1572,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int u = 0; u < U; ++u) scatter(u, dh2[u], dh1[u]);
                 const int od0 = t0 + r0 - H;  // rows od0 .. od0+U-1 are complete now
                 if (FULL && lv && od0 >= run_t0) {  // the common case: no per-row predicate
-                  IO* op = out + (obase + (uint32_t)od0 * rs32);
-#pragma unroll
+                  uint32_t oo = obase + (uint32_t)od0 * rs32;  // 32-bit element offsets: one wide
+#pragma unroll                                                // multiply-add per store address
                   for (int u = 0; u < U; ++u) {
-                    st_out(op, pacc[u], pol_out);
-                    op += rowstride;
+                    st_out(out + oo, pacc[u], pol_out);
+                    oo += rs32;
                   }
                 } else {
 #pragma unroll
