@@ -547,7 +547,10 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        key = next((kk for kk in tr if (("1>" in kk) == ("bwd" in dom_name)) and f"<{k}, {d}, float" in kk), None)
+        def _tmpl(kk):  # "psn_stream_kernel<K, D, float, BWD, SP>" -> ["K", "D", "float", "BWD", "SP"]
+            return [t.strip() for t in kk[kk.index("<") + 1:kk.rindex(">")].split(",")]
+        key = next((kk for kk in tr if _tmpl(kk)[:4] == [str(k), str(d), "float", "1" if "bwd" in dom_name else "0"]),
+                   None)
         if key is not None and args.dtype == "f32" and (T, Bl, C) == (1024, 64, 512):
             traffic = tr[key]["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
