@@ -134,9 +134,13 @@ bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
   // give every team the same number of groups (nT divides G, or nT = G).
   // Measured at the metric shape: flat from 4 to 16 teams when balanced, 25%
   // slower with 1 team or an unbalanced split (profiles/r1_sweep_teams.txt).
+  // Round 2: at most 2 groups per team when G allows (a balanced split): longer
+  // ranges measured faster than more pipelining depth (backward at the metric
+  // shape 4 -> 8 teams: 132 -> 129 us; profiles/r2_sweep_plan.txt).
   {
     int nT = (int)((6LL * p.nCTA + p.tpg - 1) / p.tpg);
     if (nT < 1) nT = 1;
+    if (nT < p.G / 2) nT = p.G / 2;
     while (nT < p.G && p.G % nT != 0) ++nT;
     if (nT > p.G) nT = p.G;
     nT = env_int(bwd ? "PSN_TEAMS_BWD" : "PSN_TEAMS_FWD", env_int("PSN_TEAMS", nT));

@@ -224,6 +224,19 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
       : "memory");
 }
 
+#ifndef PSN_RED_RELEASE
+#define PSN_RED_RELEASE 1  // 0: fence.acq_rel.gpu + relaxed red (round-1 form, A/B)
+#endif
+// arrival on a grid counter that releases this thread's prior writes (and,
+// through the preceding __syncwarp, its warp's)
+__device__ __forceinline__ void arrive_release(unsigned* a) {
+  if (PSN_RED_RELEASE) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a) : "memory");
+  } else {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a) : "memory");
+  }
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
@@ -848,8 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (lane == 0) {
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cntA + g1) : "memory");
+          arrive_release(a.cntA + g1);
         }
         // phase B: exact adds on the agreed grid (every member arrived in phase A)
         if (wk) {
@@ -866,8 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // one release fence for this group's adds, then a relaxed arrival
         __syncwarp();
         if (lane == 0) {
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + g1) : "memory");
+          arrive_release(a.cnt + g1);
         }
       }
     }
