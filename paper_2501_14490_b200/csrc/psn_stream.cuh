@@ -248,10 +248,14 @@ __device__ __forceinline__ void wait_counter(const unsigned* a, unsigned target,
                                              unsigned long long lim) {
   if (ld_acquire(a) >= target) return;
   const unsigned long long t0 = gtimer();
-  unsigned v;
-  for (unsigned n = 1; (v = ld_acquire(a)) < target; ++n) {
-    __nanosleep(128);  // short: this wait is on the critical path of every group's fold
-    if ((n & 255u) == 0 && lim && gtimer() - t0 > lim) expired(what, (int)v, (int)target);
+  for (;;) {  // bursts of cheap polls (this wait is on the critical path of every group's fold),
+              // the watchdog clock read once per burst
+#pragma unroll 1
+    for (int n = 0; n < 64; ++n) {
+      if (ld_acquire(a) >= target) return;
+      __nanosleep(256);
+    }
+    if (lim && gtimer() - t0 > lim) expired(what, (int)ld_acquire(a), (int)target);
   }
 }
 
@@ -1128,6 +1132,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          // warps whose batch row is padding (N not a multiple of 16) skip the row math
+          const bool rowv = (unsigned)(nb * kBoxN + n_in) < mN;
           if constexpr (SP) {
             if (ct != cur_ct) {
               if (tile != t_a) flush_f();
@@ -1211,7 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
-          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if ((a.ablate & 1) || !rowv) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           if (lv) {  // padding lanes (n >= N or column >= C) saw TMA zero fill; drop them
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1283,6 +1289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          // warps whose batch row is padding (N not a multiple of 16) skip the row math
+          const bool rowv = (unsigned)(nb * kBoxN + n_in) < mN;
           if constexpr (SP) {
             if (ct != cur_ct) {
               if (tile != t_a) flush_b();
@@ -1340,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < H; ++j) xd[j] = xd[j + U];
             }
           };
-          if (!(a.ablate & 1)) rows();
+          if (!(a.ablate & 1) && rowv) rows();
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
@@ -1393,6 +1401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          // warps whose batch row is padding (N not a multiple of 16) skip the row math
+          const bool rowv = (unsigned)(nb * kBoxN + n_in) < mN;
           if constexpr (SP) {
             if (ct != cur_ct) {
               ci = col_info(g, ct);
@@ -1442,7 +1452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
             }
           };
-          if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+          if ((a.ablate & 1) || !rowv) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           release_item();
           if (++tt == p.ttl) {
             tt = 0;
@@ -1539,6 +1549,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int tile = t_a; tile < t_b; ++tile) {
           const int t0 = tt * TB;
+          // warps whose batch row is padding (N not a multiple of 16) skip the row math
+          const bool rowv = (unsigned)(nb * kBoxN + n_in) < mN;
           if constexpr (SP) {
             if (ct != cur_ct) {
               ci = col_info(g, ct);
@@ -1606,7 +1618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = H; j < H + U; ++j) pacc[j] = 0.f;
               }
             };
-            if (a.ablate & 1) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
+            if ((a.ablate & 1) || !rowv) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
           }
           release_item();
           if constexpr (H > 0) {
