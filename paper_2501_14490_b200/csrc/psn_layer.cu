@@ -176,12 +176,16 @@ __device__ __forceinline__ void push(double (&xw)[K], double v) {
   xw[K - 1] = v;
 }
 
-// reference tap order: acc = 0; acc += w_i * x_i for i = 0..K-1 (mul, then add)
+// reference tap order (oldest tap first) with fused multiply-adds: for the
+// power-of-two w_q every product is exact, so the DFMA chain equals the
+// reference's mul-then-add bit for bit; for float W it differs by at most an
+// f64 ulp before the carrier rounding (the streamed kernels do the same).  The
+// engine-level operators (psn_engines.cu) keep the separate mul and add.
 template <int K>
 __device__ __forceinline__ double conv_taps(const double (&w)[K], const double (&xw)[K]) {
-  double h = 0.0;
+  double h = w[0] * xw[0];
 #pragma unroll
-  for (int i = 0; i < K; ++i) h = __dadd_rn(h, __dmul_rn(w[i], xw[i]));
+  for (int i = 1; i < K; ++i) h = fma(w[i], xw[i], h);
   return h;
 }
 
@@ -189,7 +193,7 @@ __device__ __forceinline__ double conv_taps(const double (&w)[K], const double (
 // forward pass 1: statistics of h1 = conv(x, W)
 // ------------------------------------------------------------------------------
 template <int K, typename IO>
-__global__ void __launch_bounds__(kThreads) fwd_stats_kernel(Geom g, const IO* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) fwd_stats_kernel(Geom g, const IO* __restrict__ x,
                                                              const double* __restrict__ W,
                                                              int shared,
                                                              double* __restrict__ part) {
@@ -357,7 +361,7 @@ __global__ void eval_fold_kernel(Geom g, const double* __restrict__ W, int flags
 // rounded to f32 like the reference's float32 deployment path)
 // ------------------------------------------------------------------------------
 template <int K, typename IO, int MODE>
-__global__ void __launch_bounds__(kThreads) fwd_spike_kernel(Geom g, const IO* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) fwd_spike_kernel(Geom g, const IO* __restrict__ x,
                                                              const double* __restrict__ fold,
                                                              int skind, double alpha,
                                                              IO* __restrict__ out) {
