@@ -212,6 +212,70 @@ def test_spatial_inputs_streamed_parity(shape, k, d, dt):
                          spatial=shape[3:])
 
 
+FLAG_CASES = [
+    # name, (T, N, C), k, d, flags
+    ("shared", (301, 23, 64), 3, 2, dict(shared=True)),
+    ("round_ste", (257, 20, 64), 4, 1, dict(round_ste=True)),
+    ("rational", (300, 16, 96), 4, 2, dict(surrogate="rational", alpha=10.0)),
+    ("float_weights", (200, 18, 64), 5, 1, dict(quantized=False)),
+    ("running_fusion", (250, 24, 64), 4, 3, dict(fuse_from_batch_stats=False)),
+    ("k6d3", (333, 17, 32), 6, 3, {}),
+    ("k7d2", (129, 40, 96), 7, 2, {}),
+    ("k8d1", (100, 16, 64), 8, 1, {}),
+    ("k8d3_T_lt_halo", (19, 16, 32), 8, 3, {}),
+]
+
+
+@pytest.mark.parametrize("name,shape,k,d,flags", FLAG_CASES, ids=[c[0] for c in FLAG_CASES])
+def test_streamed_flag_matrix_two_steps(name, shape, k, d, flags):
+    """The streamed kernels under every layer option the reference has (shared
+    weights, ROUND_STE, rational surrogate, float weights, running-stat fusion),
+    orders 3-8, T and N off the tile grid, random gamma / beta / running stats;
+    two steps, so the second uses the running statistics the first updated."""
+    P = _P()
+    from paper_2501_14490_b200 import _lib as L
+    T, N, C = shape
+    rng = np.random.default_rng(sum(map(ord, name)))
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=flags.get("quantized", True),
+                         weight_sharing=P.WeightSharing.SHARED if flags.get("shared") else P.WeightSharing.CHANNEL_WISE,
+                         grad_mode=P.QuantGradMode.ROUND_STE if flags.get("round_ste") else P.QuantGradMode.WHOLE_STE)
+    sur = P.SurrogateConfig(P.SurrogateKind(flags.get("surrogate", "arctan")), flags.get("alpha", 2.0))
+    layer = P.SpikingLayer(cfg, surrogate=sur, weight_init="uniform", rng=np.random.default_rng(7), device="cuda",
+                           fuse_from_batch_stats=flags.get("fuse_from_batch_stats", True))
+    gamma, beta = rng.uniform(0.5, 1.5, C), rng.uniform(-1.5, 0.5, C)
+    rm, rv = rng.normal(0.0, 0.3, C), rng.uniform(0.5, 2.0, C)
+    with torch.no_grad():
+        layer.gamma.copy_(torch.from_numpy(gamma))
+        layer.beta.copy_(torch.from_numpy(beta))
+        layer.running_mean.copy_(torch.from_numpy(rm))
+        layer.running_var.copy_(torch.from_numpy(rv))
+    desc = L.make_desc(shape, k, d, torch.float32, flags=layer._flags(P.Mode.TRAIN))
+    assert L.plan_info(desc, False)["streamed"] == 1 and L.plan_info(desc, True)["streamed"] == 1
+    p = O.init_layer(C, k, d, weight_init="uniform", rng=np.random.default_rng(7), shared=flags.get("shared", False),
+                     quantized=flags.get("quantized", True), round_ste=flags.get("round_ste", False),
+                     fuse_from_batch_stats=flags.get("fuse_from_batch_stats", True),
+                     surrogate=flags.get("surrogate", "arctan"), alpha=flags.get("alpha", 2.0))
+    p.W = layer.W.detach().cpu().numpy().copy()
+    p.gamma, p.beta, p.running_mean, p.running_var = gamma.copy(), beta.copy(), rm.copy(), rv.copy()
+    for step in range(2):
+        x_np = rng.standard_normal(shape).astype(np.float32)
+        dy_np = rng.standard_normal(shape).astype(np.float32)
+        x = torch.tensor(x_np, device="cuda", requires_grad=True)
+        layer.zero_grad(set_to_none=True)
+        out = layer(x, P.Mode.TRAIN)
+        out.backward(torch.tensor(dy_np, device="cuda"))
+        ref_out, cache, dx, dW, dg, db = O.train_step(p, x_np, dy_np)
+        st = {kk: v.cpu().numpy() for kk, v in layer.last_state().items()}
+        assert np.array_equal(st["w_q"], cache.w_q) if cfg.quantized else True
+        assert_rel(layer.running_mean.cpu().numpy(), p.running_mean, 1e-10, "running_mean")
+        assert_rel(layer.running_var.cpu().numpy(), p.running_var, 1e-10, "running_var")
+        spikes_match_except_ties(out.detach().cpu().numpy(), ref_out, x_np, cache.w_q, cache.b_f, d)
+        assert_close_scaled(x.grad.cpu().numpy(), dx, 1e-5, f"{name} step {step} dx")
+        assert_close_scaled(layer.W.grad.cpu().numpy(), dW, 1e-5, f"{name} step {step} dW")
+        assert_close_scaled(layer.gamma.grad.cpu().numpy(), dg, 1e-5, f"{name} step {step} dgamma")
+        assert_close_scaled(layer.beta.grad.cpu().numpy(), db, 1e-5, f"{name} step {step} dbeta")
+
+
 def test_bitwise_reproducible_run_to_run():
     """Fixed-order reductions, no floating-point atomics: two identical steps
     give bit-identical spikes, dx, gradients and running statistics (the
