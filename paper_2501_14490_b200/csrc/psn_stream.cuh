@@ -825,11 +825,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(p1f + (j & 1));
     };
     if (tm.ng > 0) stage_p1(0);
-    auto take_deposit = [&](int nv, double* t) {  // fixed-order sum over the 8 consumer-pair slots
-      const unsigned long long t0 = (PSN_TRACE_BUILD && a.trace) ? gtimer() : 0;
-      mbar_wait(depf, (unsigned)(nd & 1), a.wait_ns);
-      __syncwarp();
-      if (PSN_TRACE_BUILD && a.trace) tp_dep += gtimer() - t0;
+    // fixed-order sum over the 8 consumer-pair slots (the deposit of this CTA's
+    // consumers is complete: the caller saw depf's phase)
+    auto take_deposit = [&](int nv, double* t) {
 #pragma unroll
       for (int val = 0; val < kMaxNV; ++val) {
         if (val < nv) {
@@ -843,47 +841,85 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(depe);
       ++nd;
     };
-    for (int it = 0; it < iters; ++it) {
-      const bool p1 = it < tm.ng;
-      const int g1 = gid(it);
-      if (it + 1 < tm.ng) stage_p1(it + 1);
-      if (p1) {
-        if (!BWD) {
-          prev[((it & 7) * 2 + 0) * kCols + lane] = nrm;
-          prev[((it & 7) * 2 + 1) * kCols + lane] = nrv;
-          if (it + 1 < tm.ng) prefetch_stats(gid(it + 1));
-        }
-        const bool wk = worker_of(tm, it, 0) < tm.P;
-        double t[kMaxNV];
-        unsigned* em = a.emax + (size_t)g1 * NV * kCols + lane;
-        // phase A: agree on the largest exponent of each value's partials
-        if (wk) {
-          take_deposit(NV, t);
+    // Event loop (one warp, uniform control flow): the team-wide exponent
+    // agreement of group j (phase A -> every member arrived -> phase B) must
+    // not hold up this CTA's own pipeline, so the publisher stages the next
+    // groups' pass-1 parameters as soon as their slot is free and takes the next
+    // deposit while up to two groups wait for their phase B.
+    int jA = 0, jB = 0, jS = 1;
+    double tP0[kMaxNV], tP1[kMaxNV];  // partials of the groups awaiting phase B (by parity)
+    auto phaseA = [&](int j, double* t) {
+      const int g = gid(j);
+      if constexpr (!BWD) {
+        prev[((j & 7) * 2 + 0) * kCols + lane] = nrm;  // pre-update running stats of group j
+        prev[((j & 7) * 2 + 1) * kCols + lane] = nrv;
+        if (j + 1 < tm.ng) prefetch_stats(gid(j + 1));
+      }
+      if (worker_of(tm, j, 0) < tm.P) {
+        take_deposit(NV, t);
+        unsigned* em = a.emax + (size_t)g * NV * kCols + lane;
 #pragma unroll
-          for (int val = 0; val < NV; ++val)
-            if (t[val] != 0.0) atomicMax(em + val * kCols, exp_key(t[val]));
-        }
-        __syncwarp();
-        if (lane == 0) {
-          arrive_release(a.cntA + g1);
-        }
-        // phase B: exact adds on the agreed grid (every member arrived in phase A)
-        if (wk) {
-          if (lane == 0) wait_counter(a.cntA + g1, (unsigned)tm.sz, "exponent agreement", a.wait_ns);
-          __syncwarp();
-          const int lgP = tm.P > 1 ? 32 - __clz(tm.P - 1) : 0;
+        for (int val = 0; val < NV; ++val)
+          if (t[val] != 0.0) atomicMax(em + val * kCols, exp_key(t[val]));
+      }
+      __syncwarp();
+      if (lane == 0) arrive_release(a.cntA + g);
+    };
+    auto phaseB = [&](int j, const double* t) {
+      const int g = gid(j);
+      if (worker_of(tm, j, 0) < tm.P) {
+        const unsigned* em = a.emax + (size_t)g * NV * kCols + lane;
+        const int lgP = tm.P > 1 ? 32 - __clz(tm.P - 1) : 0;
 #pragma unroll
-          for (int val = 0; val < NV; ++val) {
-            const unsigned key = __ldcg(em + val * kCols);
-            if (t[val] != 0.0)
-              red_add_f64(a.acc + ((size_t)g1 * NV + val) * kCols + lane, round_to_agreed_grid(t[val], key, lgP));
-          }
+        for (int val = 0; val < NV; ++val) {
+          const unsigned key = __ldcg(em + val * kCols);
+          if (t[val] != 0.0)
+            red_add_f64(a.acc + ((size_t)g * NV + val) * kCols + lane, round_to_agreed_grid(t[val], key, lgP));
         }
-        // one release fence for this group's adds, then a relaxed arrival
-        __syncwarp();
-        if (lane == 0) {
-          arrive_release(a.cnt + g1);
+      }
+      __syncwarp();
+      if (lane == 0) arrive_release(a.cnt + g);  // releases this group's adds
+    };
+    unsigned long long tl0 = 0;  // start of the current idle stretch (watchdog)
+    unsigned idle = 0;
+    while (jB < tm.ng) {
+      bool prog = false;
+      // (1) pass-1 parameters of group jS once the consumers released its slot (group jS - 2)
+      if (jS < tm.ng && jS <= jA + 1) {
+        const bool fr = jS < 2 || __all_sync(0xffffffffu, mbar_try(p1e + (jS & 1), (unsigned)(((jS >> 1) - 1) & 1)));
+        if (fr) {
+          stage_p1(jS);
+          ++jS;
+          prog = true;
         }
+      }
+      // (2) phase A of group jA: its deposit is in (or this CTA has no tiles of it)
+      if (jA < tm.ng && jA < jB + 2) {
+        const bool wk = worker_of(tm, jA, 0) < tm.P;
+        const bool in = !wk || __all_sync(0xffffffffu, mbar_try(depf, (unsigned)(nd & 1)));
+        if (in) {
+          if (jA & 1) phaseA(jA, tP1); else phaseA(jA, tP0);
+          ++jA;
+          prog = true;
+        }
+      }
+      // (3) phase B of group jB once every member arrived in its phase A
+      if (jB < jA) {
+        unsigned v = 0;
+        if (lane == 0) v = ld_acquire(a.cntA + gid(jB));
+        v = __shfl_sync(0xffffffffu, v, 0);
+        if (v >= (unsigned)tm.sz) {
+          if (jB & 1) phaseB(jB, tP1); else phaseB(jB, tP0);
+          ++jB;
+          prog = true;
+        }
+      }
+      if (prog) {
+        idle = 0;
+      } else {
+        if (idle++ == 0) tl0 = gtimer();
+        __nanosleep(64);
+        if ((idle & 4095u) == 0 && a.wait_ns && gtimer() - tl0 > a.wait_ns) expired("publisher", jA, jB);
       }
     }
     if (PSN_TRACE_BUILD && a.trace && lane == 0)
