@@ -58,7 +58,7 @@ constexpr int kMaxH = 24;                        // largest (k-1)*d on this path
 constexpr int kRowBlock = 4;                     // time rows a consumer thread advances at once (ILP)
 // ... per pass (forward pass 1 / 2, backward pass 1 / 2); each must divide the tile rows
 #ifndef PSN_U_F1
-#define PSN_U_F1 4
+#define PSN_U_F1 2  // round 2: 2 (fewer live registers beside the f32 data-sum window; fwd -2.3 us)
 #endif
 #ifndef PSN_U_F2
 #define PSN_U_F2 4

@@ -23,6 +23,7 @@ dtype float32, bfloat16 or float64; outputs have the dtype of ``x``.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
 from enum import Enum
 
 import numpy as np
@@ -39,6 +40,19 @@ class Mode(Enum):
     TRAIN = "train"
     SMOOTH = "smooth"
     EVAL = "eval"
+
+
+@dataclass(frozen=True)
+class LayerMethod:
+    """One implementation choice of a layer (network.py:58-64).  Here there is
+    one fused kernel family; the planner picks the streamed persistent kernels
+    or the generic three-launch kernels from the shape, so the only candidate
+    is "stream" (the reference's engine registry is a CPU stand-in for GPU
+    methods, out of scope: SURVEY.md section 2)."""
+
+    name: str = "stream"
+    engine: object = None
+    block_size: int | None = None
 
 
 def _surrogate_code(s: SurrogateConfig) -> int:
@@ -61,6 +75,7 @@ class _PSNFunction(torch.autograd.Function):
         ctx.desc_args = desc_args
         if layer is not None:
             layer.last_fold = fold
+            layer._last = (x.detach(), desc_args)  # what the explicit backward(dy) consumes
         return out
 
     @staticmethod
@@ -104,10 +119,50 @@ class SpikingLayer(nn.Module):
         self.fuse_from_batch_stats = fuse_from_batch_stats
         self.quantize_in_smooth_mode = False
         self.last_fold = None
+        self._last = None
+        self.method = LayerMethod("stream")
 
     # -- reference-compatible helpers (network.py:162-209) ----------------------
     def out_channels(self) -> int:
         return self.cfg.channels
+
+    def parameters_list(self) -> list:
+        """[W, gamma, beta], the reference's parameters() order."""
+        return [self.W, self.gamma, self.beta]
+
+    def method_candidates(self, layout=None) -> list:
+        return [LayerMethod("stream")]
+
+    def configure(self, method: LayerMethod) -> None:
+        if method.name != "stream":
+            raise ValueError(f"unknown layer method {method.name!r} (the fused kernels are the only method)")
+        self.method = method
+
+    def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        """Explicit backward of the last TRAIN / SMOOTH forward, as the
+        reference's SpikingLayer.backward(dy) (network.py:272-318): gradients
+        ACCUMULATE into W.grad, gamma.grad, beta.grad; returns dx (dtype of x).
+        (Autograd through forward() is the usual route; this one serves code
+        written against the reference's layer-by-layer backward.)"""
+        if getattr(self, "_last", None) is None or self.last_fold is None:
+            raise RuntimeError("backward() before a TRAIN / SMOOTH forward")
+        x, desc_args = self._last
+        desc = L.make_desc(x.shape, *desc_args)
+        dy = dy.to(x.dtype).contiguous()
+        if tuple(dy.shape) != tuple(x.shape):
+            raise ValueError(f"dy has shape {tuple(dy.shape)}, the forward's input {tuple(x.shape)}")
+        dx = torch.empty_like(x)
+        dW, dg, db = torch.empty_like(self.W), torch.empty_like(self.gamma), torch.empty_like(self.gamma)
+        ws = L.workspace_for(desc, x.device, L.stream_of(x))
+        L.run(x, "psn_backward", ctypes.byref(desc), L.ptr(x), L.ptr(dy), L.ptr(self.W), L.ptr(self.gamma),
+              L.ptr(self.last_fold), L.ptr(dx), L.ptr(dW), L.ptr(dg), L.ptr(db), L.ptr(ws), L.stream_of(x))
+        with torch.no_grad():
+            for p, g in ((self.W, dW), (self.gamma, dg), (self.beta, db)):
+                if p.grad is None:
+                    p.grad = g
+                else:
+                    p.grad.add_(g)
+        return dx
 
     def _flags(self, mode: Mode) -> int:
         f = 0

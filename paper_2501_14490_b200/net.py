@@ -157,7 +157,17 @@ class SpikingNet(nn.Module):
         h = x
         for layer in self.layers:
             h = layer(h, mode)
+        self._last_out = h if mode is not Mode.EVAL else None
         return h
+
+    def backward(self, dlogits: torch.Tensor):
+        """Explicit backward of the last TRAIN / SMOOTH forward from the logits'
+        gradient (network.py:474-478); gradients accumulate into .grad."""
+        out = getattr(self, "_last_out", None)
+        if out is None:
+            raise RuntimeError("backward() before a TRAIN / SMOOTH forward")
+        out.backward(torch.as_tensor(dlogits, dtype=out.dtype, device=out.device))
+        self._last_out = None
 
     def loss(self, x: torch.Tensor, labels: torch.Tensor, mode: Mode = Mode.TRAIN):
         """Forward + cross entropy; returns (loss, accuracy) tensors."""

@@ -190,6 +190,29 @@ def test_graphed_train_step_equals_eager():
         assert torch.equal(a, b)
 
 
+def test_explicit_layer_backward_matches_autograd():
+    """SpikingLayer.backward(dy) (the reference's layer-by-layer API) returns
+    autograd's dx and accumulates the same parameter gradients."""
+    import paper_2501_14490_b200 as P
+    cfg = P.NeuronConfig(channels=64, order=4, dilation=2, quantized=True)
+    a = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(2), device="cuda")
+    b = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(2), device="cuda")
+    x = torch.randn(200, 12, 64, device="cuda")
+    dy = torch.randn(200, 12, 64, device="cuda")
+    xa = x.clone().requires_grad_(True)
+    a(xa, P.Mode.TRAIN).backward(dy)
+    b(x, P.Mode.TRAIN)
+    dx = b.backward(dy)
+    assert torch.equal(dx, xa.grad)
+    for pa, pb in zip(a.parameters_list(), b.parameters_list()):
+        assert torch.equal(pa.grad, pb.grad)
+    b.backward(dy)  # accumulates like the reference's +=
+    assert torch.equal(b.W.grad, 2 * a.W.grad)
+    assert [m.name for m in b.method_candidates()] == ["stream"]
+    with pytest.raises(ValueError):
+        b.configure(P.layer.LayerMethod("matmul"))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
