@@ -70,6 +70,10 @@ constexpr int kRowBlock = 4;                     // time rows a consumer thread 
 #define PSN_U_B2 4
 #endif
 
+#ifndef PSN_F2_FILTER
+#define PSN_F2_FILTER 1  // forward pass 2 decides spikes in f32 outside the tie band (exact f64 inside)
+#endif
+
 #ifndef PSN_B1_ALT
 #define PSN_B1_ALT 1  // backward pass 1: alternate rows between two f64 accumulator sets (ILP)
 #endif
@@ -1418,8 +1422,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       IO* out = (IO*)a.out;
       if constexpr (!BWD) {
         // ---- forward pass 2: spikes = [f32(sum_i w_q,i x[t-off_i] + b_f) >= 0]
+        // The sign is decided in f32 (the FP64 pipe bounds this pass otherwise):
+        // with power-of-two taps every product is exact, so the f32 chain hf is
+        // within (K+1) 2^-24 (|b_f| + sum |w_q x|) of the exact membrane h; where
+        // |hf| exceeds 4x that bound, sign(hf) = sign(h) = the reference's spike.
+        // Rows inside the bound (a threshold tie band, ~1e-6 of random rows) take
+        // the exact f64 chain -- warp-uniformly, for the rows that need it.
         constexpr int U = PSN_U_F2;
-        double wq[K], xw[H + U], bf = 0.0;
+        double wq[K], bf = 0.0;
+        float wqf[K], wqa[K], bff = 0.f, bfa = 0.f, xf[H + U];
         int nbi = t_a / p.ttl, tt = t_a - nbi * p.ttl;
         int ct, nb;
         sbsplit(nbi, ct, nb);
@@ -1428,9 +1439,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto params_f2 = [&]() {  // the lane's channel parameters for this column tile
           const double* pd = (const double*)(p2b + ci.chl * LY.pstride);
 #pragma unroll
-          for (int i = 0; i < K; ++i) wq[i] = ldsd(pd + i);
+          for (int i = 0; i < K; ++i) {
+            wq[i] = ldsd(pd + i);
+            wqf[i] = (float)wq[i];  // exact: a power of two in [2^-16, 2^15] (or a float weight: rounded,
+            wqa[i] = fabsf(wqf[i]);  // its error is inside the bound's factor-4 margin only if quantized)
+          }
           bf = ldsd(pd + K);
+          bff = (float)bf;
+          bfa = fabsf(bff);
         };
+        // the filter's error bound assumes exact products: power-of-two taps only
+        const bool filt = PSN_F2_FILTER && (a.flags & PSN_QUANTIZED);
         if constexpr (!SP) {
           ci = col_info(g, 0);
           params_f2();
@@ -1451,13 +1470,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool lv = (unsigned)n < mN && ci.valid;
           if (tile == t_a || tt == 0) {
 #pragma unroll
-            for (int j = 0; j < H + U; ++j) xw[j] = 0.0;
+            for (int j = 0; j < H + U; ++j) xf[j] = 0.f;
           }
           if constexpr (H > 0) if (tile == t_a && t0 > 0) {
             const uint32_t st = wait_item();
             const uint32_t xs = st;
 #pragma unroll
-            for (int r = 0; r < H; ++r) xw[r] = (double)ldsx<IO>(xs + (r) * RSB);
+            for (int r = 0; r < H; ++r) xf[r] = ldsx<IO>(xs + (r) * RSB);
             release_item();
           }
           const uint32_t st = wait_item();
@@ -1469,23 +1488,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int r0 = 0; r0 < TB; r0 += U) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) xw[H + u] = (double)ldsx<IO>(xs + ((r0 + u)) * RSB);
-              double h[U];  // power-of-two products are exact: DFMA == the reference's mul-then-add
-#pragma unroll
-              for (int u = 0; u < U; ++u) h[u] = wq[0] * xw[u + slot<K, D>(0)];
-#pragma unroll
-              for (int i = 1; i < K; ++i)
-#pragma unroll
-                for (int u = 0; u < U; ++u) h[u] = fma(wq[i], xw[u + slot<K, D>(i)], h[u]);
+              for (int u = 0; u < U; ++u) xf[H + u] = ldsx<IO>(xs + ((r0 + u)) * RSB);
+              float sp[U];
+              bool need = false, nd_u[U];
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
-                const float sp = __dadd_rn(h[u], bf) >= -0x1p-150 ? 1.0f : 0.0f;
-                if (lv && (FULL || r0 + u < nvalid)) st_out(out + ooff, sp, pol_out);
+                float hf = bff, sf = bfa;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                  hf = fmaf(wqf[i], xf[u + slot<K, D>(i)], hf);
+                  sf = fmaf(wqa[i], fabsf(xf[u + slot<K, D>(i)]), sf);
+                }
+                nd_u[u] = !filt || !(fabsf(hf) > fmaf(sf, (float)(4 * (K + 1)) * 0x1p-24f, 0x1p-126f));
+                need |= nd_u[u];
+                sp[u] = hf >= 0.f ? 1.0f : 0.0f;
+              }
+              if (__any_sync(0xffffffffu, need)) {  // exact membrane for the rows inside the tie band
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                  if (nd_u[u]) {  // power-of-two products are exact: DFMA == the reference's mul-then-add
+                    double h = wq[0] * (double)xf[u + slot<K, D>(0)];
+#pragma unroll
+                    for (int i = 1; i < K; ++i) h = fma(wq[i], (double)xf[u + slot<K, D>(i)], h);
+                    // Heaviside on the f32-rounded membrane: f32(h) >= 0  <=>  h >= -2^-150
+                    sp[u] = __dadd_rn(h, bf) >= -0x1p-150 ? 1.0f : 0.0f;
+                  }
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                if (lv && (FULL || r0 + u < nvalid)) st_out(out + ooff, sp[u], pol_out);
                 ooff += rs32;
               }
 #pragma unroll
-              for (int j = 0; j < H; ++j) xw[j] = xw[j + U];
+              for (int j = 0; j < H; ++j) xf[j] = xf[j + U];
             }
           };
           if ((a.ablate & 1) || !rowv) {} else if (nvalid == TB) rows(std::true_type{}); else rows(std::false_type{});
