@@ -178,6 +178,7 @@ class SpikingNet(nn.Module):
         self.zero_grad()
         loss, acc = self.loss(x, labels, mode)
         loss.backward()
+        self._last_out = None  # release the autograd graph (and its AccumulateGrad nodes' stream)
         return loss.detach(), acc
 
     def train_step_grads(self, x: torch.Tensor, labels: torch.Tensor, mode: Mode = Mode.TRAIN):
