@@ -69,7 +69,10 @@ typedef enum {
   PSN_USE_BATCH_STATS = 4,         /* SpikingLayer.fuse_from_batch_stats           */
   PSN_SMOOTH = 8,                  /* Mode.SMOOTH: primitive output, stats frozen  */
   PSN_QUANTIZE_IN_SMOOTH = 16,     /* SpikingLayer.quantize_in_smooth_mode         */
-  PSN_ROUND_STE = 32               /* QuantGradMode.ROUND_STE (else WHOLE_STE)     */
+  PSN_ROUND_STE = 32,              /* QuantGradMode.ROUND_STE (else WHOLE_STE)     */
+  PSN_GENERIC = 64                 /* force the three-launch kernels (no streamed  */
+                                   /* kernel); part of the descriptor so that the  */
+                                   /* workspace size and the call agree            */
 } psn_flag_t;
 
 typedef struct {

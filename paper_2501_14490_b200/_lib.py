@@ -26,6 +26,7 @@ PSN_USE_BATCH_STATS = 4
 PSN_SMOOTH = 8
 PSN_QUANTIZE_IN_SMOOTH = 16
 PSN_ROUND_STE = 32
+PSN_GENERIC = 64
 PSN_FOLD_HDR = 7
 
 

@@ -101,6 +101,202 @@ __device__ __forceinline__ double load_wide(const double* p) { return __ldg(p); 
 __device__ __forceinline__ double load_wide(const __nv_bfloat16* p) {
   return (double)__bfloat162float(__ldg(p));
 }
+// the same on register values (prefetched raw carrier elements)
+__device__ __forceinline__ double wide(float v) { return (double)v; }
+__device__ __forceinline__ double wide(double v) { return v; }
+__device__ __forceinline__ double wide(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+__device__ __forceinline__ float as_f(float v) { return v; }
+__device__ __forceinline__ float as_f(double v) { return (float)v; }
+__device__ __forceinline__ float as_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename IO>
+__device__ __forceinline__ IO io_zero() { return IO(0); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 io_zero<__nv_bfloat16>() { return __float2bfloat16_rn(0.0f); }
+
+// Walk one column of x (and dy when DY) over subsequence steps [t0, t1) with
+// U loads of each stream in flight: f(xv, dyv, t, eo) runs for every step in
+// order, eo = (t - t0) * step the step's element offset from px; steps at or
+// beyond `lim` (or an invalid column) read as zero.  px / pq point at step t0,
+// consecutive steps are `step` elements apart.  The U-deep register prefetch
+// keeps enough bytes in flight per SM for HBM (a load consumed by the next
+// instruction stalls the warp for the full memory latency); full chunks of U
+// steps call f unconditionally so the callers' shifting register windows are
+// renamed rather than moved.
+template <int U, bool DY, typename IO, typename F>
+__device__ __forceinline__ void stream_col(const IO* px, const IO* pq, int64_t step, int64_t t0,
+                                           int64_t t1, int64_t lim, bool jv, F&& f) {
+  IO bx[U], bq[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = jv && t0 + u < lim;
+    bx[u] = ok ? __ldg(px + u * step) : io_zero<IO>();
+    bq[u] = (DY && ok) ? __ldg(pq + u * step) : io_zero<IO>();
+  }
+  const int64_t ustep = (int64_t)U * step;
+  int64_t t = t0, eo = 0;
+  for (; t + U <= t1; t += U) {
+    IO cx[U], cq[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cx[u] = bx[u];
+      cq[u] = bq[u];
+    }
+    const IO* nx = px + eo + ustep;
+    const IO* nq = pq + eo + ustep;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = jv && t + U + u < lim;
+      bx[u] = ok ? __ldg(nx + u * step) : io_zero<IO>();
+      bq[u] = (DY && ok) ? __ldg(nq + u * step) : io_zero<IO>();
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) f(cx[u], cq[u], t + u, eo + u * step);
+    eo += ustep;
+  }
+  // tail (< U steps): already in bx / bq
+#pragma unroll
+  for (int u = 0; u < U - 1; ++u)
+    if (t + u < t1) f(bx[u], bq[u], t + u, eo + u * step);
+}
+
+// ---- per-warp shared-memory ring (cp.async) -------------------------------------
+// Each lane copies ITS OWN column element of every step into the warp's ring
+// and later reads it back itself, so no lane-to-lane synchronisation is needed
+// (cp.async.wait_group is per thread).  CH steps per commit group (also the
+// compute unroll), kRingSteps / CH groups in the ring, all but one in flight:
+// kRingSteps - CH steps of every stream in flight per warp without holding
+// registers.
+constexpr int kRingSteps = 32;
+
+template <typename IO>
+__host__ __device__ constexpr bool ring_streamed() { return sizeof(IO) >= 4; }  // cp.async moves 4 / 8 / 16 B
+template <typename IO>
+__host__ __device__ constexpr size_t ring_bytes(int streams) {  // dynamic shared memory of one block
+  return ring_streamed<IO>() ? (size_t)streams * kWarps * kRingSteps * 32 * sizeof(IO) : 0;
+}
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* sdst, const void* gsrc, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  const int n = ok ? BYTES : 0;  // 0 source bytes: the destination is zero-filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// A lane's view of its 32-column tile: its lane index, whether its own column
+// exists, how many columns of the tile exist, and whether the tile's rows may
+// be moved as 16-byte pieces (every stream 16-B aligned, J a multiple of the
+// elements per piece, so a piece is wholly inside or outside the tile).
+struct ColTile {
+  int lane, nvalid;
+  bool jv, vec;
+};
+template <typename IO>
+__device__ __forceinline__ ColTile col_tile(const Geom& g, const void* a, const void* b) {
+  ColTile t;
+  t.lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  t.nvalid = (int)(g.J - j0 < 32 ? g.J - j0 : 32);
+  t.jv = t.lane < t.nvalid;
+  t.vec = (g.J % (16 / (int)sizeof(IO)) == 0) && ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
+  return t;
+}
+
+// stream_col through the ring: rx / rq are this warp's rings ([kRingSteps][32]
+// elements each), gx / gq any valid global address (source of the zero-byte
+// copies for steps that read as zero).  Scalar mode: every lane copies its own
+// column (no lane-to-lane hand-off).  Vector mode: 16-B pieces, 32 / (16 / es)
+// lanes per step row, lanes read rows other lanes copied, so the warp
+// synchronises after each wait and before each refill.
+template <int kRingCH, bool DY, typename IO, typename F>
+__device__ __forceinline__ void stream_ring(IO* rx, IO* rq, const ColTile& ct, const IO* px, const IO* pq,
+                                            const IO* gx, const IO* gq, int64_t step, int64_t t0,
+                                            int64_t t1, int64_t lim, F&& f) {
+  constexpr int kRingN = kRingSteps / kRingCH;
+  constexpr int EPP = 16 / (int)sizeof(IO);  // elements per 16-B piece
+  constexpr int LPS = 32 / EPP;              // lanes per step row
+  constexpr int SPI = 32 / LPS;              // step rows per warp-wide copy
+  static_assert(kRingCH % SPI == 0, "chunk must be a multiple of the rows per copy");
+  const int lane = ct.lane;
+  const int nchunks = (int)((t1 - t0 + kRingCH - 1) / kRingCH);
+  const int64_t cstep = (int64_t)kRingCH * step;
+  // vector mode: this lane copies piece pc of rows su, su + SPI, ...
+  const int su = lane / LPS, pc = lane % LPS;
+  const bool pok = pc * EPP < ct.nvalid;
+  const IO* vx = px - lane + pc * EPP;  // tile start + piece
+  const IO* vq = pq - lane + pc * EPP;
+  int64_t ie = 0;  // element offset (from px) of the next chunk to issue
+  int ic = 0;      // next chunk to issue
+  auto issue = [&]() {
+    if (ic < nchunks) {
+      const int base = (ic & (kRingN - 1)) * kRingCH;
+      const int64_t tb = t0 + (int64_t)ic * kRingCH;
+      if (ct.vec) {
+#pragma unroll
+        for (int u0 = 0; u0 < kRingCH; u0 += SPI) {
+          const int u = u0 + su;
+          const bool ok = pok && tb + u < lim;
+          const int64_t e = ie + u * step;
+          cp_async_elem<16>(rx + (base + u) * 32 + pc * EPP, ok ? vx + e : gx, ok);
+          if (DY) cp_async_elem<16>(rq + (base + u) * 32 + pc * EPP, ok ? vq + e : gq, ok);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kRingCH; ++u) {
+          const bool ok = ct.jv && tb + u < lim;
+          const int64_t e = ie + u * step;
+          cp_async_elem<sizeof(IO)>(rx + (base + u) * 32 + lane, ok ? px + e : gx, ok);
+          if (DY) cp_async_elem<sizeof(IO)>(rq + (base + u) * 32 + lane, ok ? pq + e : gq, ok);
+        }
+      }
+    }
+    cp_async_commit();
+    ++ic;
+    ie += cstep;
+  };
+#pragma unroll
+  for (int c = 0; c < kRingN - 1; ++c) issue();
+  int64_t eo = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    if (ct.vec) __syncwarp();  // every lane is done with the slot about to be refilled
+    issue();
+    cp_async_wait<kRingN - 1>();
+    if (ct.vec) __syncwarp();  // rows copied by other lanes are visible
+    const int base = (c & (kRingN - 1)) * kRingCH;
+    const int64_t tc = t0 + (int64_t)c * kRingCH;
+    const IO* sx = rx + base * 32 + lane;
+    const IO* sq = rq + base * 32 + lane;
+    if (tc + kRingCH <= t1) {
+#pragma unroll
+      for (int u = 0; u < kRingCH; ++u) f(sx[u * 32], DY ? sq[u * 32] : io_zero<IO>(), tc + u, eo + u * step);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kRingCH; ++u)
+        if (tc + u < t1) f(sx[u * 32], DY ? sq[u * 32] : io_zero<IO>(), tc + u, eo + u * step);
+    }
+    eo += cstep;
+  }
+  cp_async_wait<0>();
+  if (ct.vec) __syncwarp();  // the ring is reused by the warp's next segment
+}
+
+// the streaming loop of the generic kernels: the shared-memory ring for 4 / 8 B
+// carriers, the register prefetch for bf16.  `ring` is this warp's slice of
+// the block's dynamic shared memory (2 streams when DY).  CH: steps per
+// chunk (unrolled; 4 for the register-heavy high orders).
+template <int CH, bool DY, typename IO, typename F>
+__device__ __forceinline__ void stream_any(IO* ring, const ColTile& ct, const IO* px, const IO* pq, const IO* gx,
+                                           const IO* gq, int64_t step, int64_t t0, int64_t t1, int64_t lim,
+                                           F&& f) {
+  if constexpr (ring_streamed<IO>())
+    stream_ring<CH, DY>(ring, ring + kRingSteps * 32, ct, px, pq, gx, gq, step, t0, t1, lim, f);
+  else
+    stream_col<4, DY>(px, pq, step, t0, t1, lim, ct.jv, f);
+}
+
 __device__ __forceinline__ float load_f(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float load_f(const double* p) { return (float)__ldg(p); }
 __device__ __forceinline__ float load_f(const __nv_bfloat16* p) {
@@ -151,6 +347,14 @@ __device__ __forceinline__ float rcp_approx(float v) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
   return r;
 }
+// 1/v to ~2^-44 relative: MUFU.RCP64H seed (~2^-22) and one Newton step
+__device__ __forceinline__ double rcp_f64(double v) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  const double e = fma(-v, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ float surrogate_grad(const Surrogate& s, float h) {
   const float t = s.c * h;
   return s.scale * rcp_approx(fmaf(t, s.kind == PSN_ARCTAN ? t : h, 1.0f));

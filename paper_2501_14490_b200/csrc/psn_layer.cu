@@ -63,8 +63,8 @@ Geom plan(const psn_desc_t* desc) {
   while (L > 16 && g.ctiles * g.N * g.d * ((g.S + L - 1) / L) < target_warps) L >>= 1;
   if (L > g.S) L = g.S;
   if (L < 1) L = 1;
-  g.L = L;
   g.nch = (g.S + L - 1) / L;
+  g.L = (g.S + g.nch - 1) / g.nch;  // equal chunks: a warp's segments are all about as long
   g.nseg = g.N * g.d * g.nch;
   int spw = 1;
   while (spw < 64 && g.ctiles * ((g.nseg + kWarps * spw * 2 - 1) / (kWarps * spw * 2)) * kWarps >= target_warps)
@@ -77,7 +77,7 @@ Geom plan(const psn_desc_t* desc) {
 }
 
 struct WsLayout {
-  size_t part1, part3, bfold, dwtmp, evalfold, fused, total;
+  size_t part1, part3, bfold, dwtmp, evalfold, fused, dhm, dhm_bytes, total;
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -98,6 +98,14 @@ WsLayout ws_layout(const psn_desc_t* desc) {
   off = align256(off + sizeof(double) * PSN_FOLD_STRIDE((size_t)g.k) * g.C);
   w.fused = off;
   off = align256(off + stream::workspace_bytes(desc));
+  // generic backward of a 4 / 2 B carrier: dh2 and h1 - mu materialised as f32
+  // by bwd_reduce for an FP32-only bwd_dx_mat.  Sized from the shape alone (never
+  // from run-time knobs): a streamable shape that still takes the generic path
+  // recomputes them instead (bwd_dx_kernel).
+  w.dhm = off;
+  w.dhm_bytes = (desc->dtype != PSN_F64 && !stream::shape_eligible(desc))
+                    ? 2 * sizeof(float) * (size_t)desc->T * desc->N * desc->C * desc->Q : 0;
+  off = align256(off + w.dhm_bytes);
   w.total = off;
   return w;
 }
@@ -193,7 +201,7 @@ __device__ __forceinline__ double conv_taps(const double (&w)[K], const double (
 // forward pass 1: statistics of h1 = conv(x, W)
 // ------------------------------------------------------------------------------
 template <int K, typename IO>
-__global__ void __launch_bounds__(kThreads, 2) fwd_stats_kernel(Geom g, const IO* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_stats_kernel(Geom g, const IO* __restrict__ x,
                                                              const double* __restrict__ W,
                                                              int shared,
                                                              double* __restrict__ part) {
@@ -205,6 +213,9 @@ __global__ void __launch_bounds__(kThreads, 2) fwd_stats_kernel(Geom g, const IO
 #pragma unroll
   for (int i = 0; i < K; ++i) w[i] = jv ? W[(shared ? 0 : c) * K + i] : 0.0;
   const int64_t step = (int64_t)g.d * g.row;
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  IO* ring = reinterpret_cast<IO*>(psn_dsm) + warp * kRingSteps * 32;
+  const ColTile ct = col_tile<IO>(g, x, x);
   Moments acc{0.0, 0.0, 0.0};
   for (int sp = 0; sp < g.spw; ++sp) {
     const int64_t seg = ((int64_t)blockIdx.y * g.spw + sp) * kWarps + warp;
@@ -215,18 +226,15 @@ __global__ void __launch_bounds__(kThreads, 2) fwd_stats_kernel(Geom g, const IO
     double xw[K];
     prime_window<K>(xw, base, step, s.s0, jv);
     const IO* p = base + s.s0 * step;
-    push<K>(xw, jv ? load_wide(p) : 0.0);
-    const double k0 = Carrier<IO>::round(conv_taps<K>(w, xw));  // shift for the moments
-    double s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int64_t t = s.s0 + 1; t < s.s1; ++t) {
-      p += step;
-      push<K>(xw, jv ? load_wide(p) : 0.0);
+    double k0 = 0.0, s1 = 0.0, s2 = 0.0;  // k0: the segment's first h1, shift for the moments
+    stream_any<(K > 8 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t t, int64_t) {
+      push<K>(xw, wide(xv));
       const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
+      if (t == s.s0) k0 = h1;
       const double dl = h1 - k0;
       s1 += dl;
       s2 = fma(dl, dl, s2);
-    }
+    });
     const double n = (double)(s.s1 - s.s0);
     Moments m{n, k0 + s1 / n, fmax(s2 - s1 * s1 / n, 0.0)};
     acc = merge(acc, m);
@@ -361,7 +369,7 @@ __global__ void eval_fold_kernel(Geom g, const double* __restrict__ W, int flags
 // rounded to f32 like the reference's float32 deployment path)
 // ------------------------------------------------------------------------------
 template <int K, typename IO, int MODE>
-__global__ void __launch_bounds__(kThreads, 2) fwd_spike_kernel(Geom g, const IO* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_spike_kernel(Geom g, const IO* __restrict__ x,
                                                              const double* __restrict__ fold,
                                                              int skind, double alpha,
                                                              IO* __restrict__ out) {
@@ -375,6 +383,9 @@ __global__ void __launch_bounds__(kThreads, 2) fwd_spike_kernel(Geom g, const IO
   for (int i = 0; i < K; ++i) wq[i] = jv ? f[PSN_FOLD_HDR + K + i] : 0.0;
   const double bf = jv ? f[3] : 0.0;
   const int64_t step = (int64_t)g.d * g.row;
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  IO* ring = reinterpret_cast<IO*>(psn_dsm) + warp * kRingSteps * 32;
+  const ColTile ct = col_tile<IO>(g, x, x);
   for (int64_t seg = (int64_t)blockIdx.y * kWarps + warp; seg < g.nseg;
        seg += (int64_t)gridDim.y * kWarps) {
     Seg s;
@@ -393,22 +404,20 @@ __global__ void __launch_bounds__(kThreads, 2) fwd_spike_kernel(Geom g, const IO
     }
     const IO* p = base + s.s0 * step;
     IO* o = out + off + s.s0 * step;
-#pragma unroll 4
-    for (int64_t t = s.s0; t < s.s1; ++t) {
-      double v = jv ? load_wide(p) : 0.0;
+    stream_any<(K > 8 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t, int64_t eo) {
+      double v = wide(xv);
       if (MODE == 2) v = Carrier<IO>::to_f32(v);
       push<K>(xw, v);
       double h = __dadd_rn(conv_taps<K>(wq, xw), bf);
       h = (MODE == 2) ? (double)(float)h : Carrier<IO>::round(h);
       if (jv) {
+        IO* ot = o + eo;
         if (MODE == 1)
-          Carrier<IO>::store(o, surrogate_primitive(skind, alpha, h));
+          Carrier<IO>::store(ot, surrogate_primitive(skind, alpha, h));
         else
-          Carrier<IO>::storef(o, h >= 0.0 ? 1.0f : 0.0f);
+          Carrier<IO>::storef(ot, h >= 0.0 ? 1.0f : 0.0f);
       }
-      p += step;
-      o += step;
-    }
+    });
   }
 }
 
@@ -416,12 +425,14 @@ __global__ void __launch_bounds__(kThreads, 2) fwd_spike_kernel(Geom g, const IO
 // backward pass 1: per-column reductions
 // part3 layout: [rows][3K+1][J]: db, dwq[0..K), sx[0..K), sxc[0..K)
 // ------------------------------------------------------------------------------
+// dh2 = dy * sigma'(h2) on a prefetched dy element, in f64 like the reference
+// (surrogate.py:36-38): the float64 carrier with the reference's own
+// expressions, the f32 / bf16 carriers with a 2^-44-accurate reciprocal (an f32
+// sigma' is off by up to an ulp per element, and the per-channel sums of
+// 10^5..10^7 such terms drift by ~1e-5 relative)
 template <typename IO>
-__device__ __forceinline__ double dh2_of(const Surrogate& sur, int skind, double alpha, double h2,
-                                         const IO* dyp) {
+__device__ __forceinline__ double dh2_val(const Surrogate& sur, int skind, double alpha, double h2, IO dyr) {
   if constexpr (std::is_same<IO, double>::value) {
-    // float64 carrier: the reference's own f64 expressions (surrogate.py:36-38)
-    const double dyv = __ldg(dyp);
     double sg;
     if (skind == PSN_ARCTAN) {
       const double u = 0.5 * 3.141592653589793 * alpha * h2;
@@ -429,9 +440,13 @@ __device__ __forceinline__ double dh2_of(const Surrogate& sur, int skind, double
     } else {
       sg = 1.0 / (1.0 + alpha * h2 * h2);
     }
-    return dyv * sg;
+    return dyr * sg;
   } else {
-    return (double)(load_f(dyp) * surrogate_grad(sur, (float)h2));
+    if (skind == PSN_ARCTAN) {
+      const double u = (0.5 * 3.141592653589793 * alpha) * h2;
+      return wide(dyr) * (0.5 * alpha) * rcp_f64(fma(u, u, 1.0));
+    }
+    return wide(dyr) * rcp_f64(fma(alpha * h2, h2, 1.0));
   }
 }
 
@@ -442,7 +457,8 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
                                                               int shared,
                                                               const double* __restrict__ fold,
                                                               Surrogate sur, int skind, double alpha,
-                                                              double* __restrict__ part) {
+                                                              double* __restrict__ part,
+                                                              float* __restrict__ dhm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const bool jv = j < g.J;
@@ -457,9 +473,20 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
   const double bf = jv ? f[3] : 0.0;
   const double mu = jv ? f[0] : 0.0;
   const int64_t step = (int64_t)g.d * g.row;
-  double db = 0.0, dwq[K], sx[K], sxc[K];
+  // sx[i] = sum_t x[t - (K-1-i)] is not accumulated per step: it is the
+  // column's total minus, for every residue subsequence, its last K-1-i
+  // values (taken from the window at the subsequence's end, kept in shared
+  // memory; x before the stream start is zero).
+  __shared__ double tails[K > 1 ? K - 1 : 1][kWarps][32];
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  IO* ring = reinterpret_cast<IO*>(psn_dsm) + warp * 2 * kRingSteps * 32;
+  const ColTile ct = col_tile<IO>(g, x, dy);
+  const int64_t nel = g.T * g.row;
 #pragma unroll
-  for (int i = 0; i < K; ++i) dwq[i] = sx[i] = sxc[i] = 0.0;
+  for (int i = 0; i < K - 1; ++i) tails[i][warp][lane] = 0.0;
+  double db = 0.0, xsum = 0.0, dwq[K], sxc[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) dwq[i] = sxc[i] = 0.0;
   for (int sp = 0; sp < g.spw; ++sp) {
     const int64_t seg = ((int64_t)blockIdx.y * g.spw + sp) * kWarps + warp;
     if (seg >= g.nseg) break;
@@ -470,22 +497,33 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
     prime_window<K>(xw, x + off, step, s.s0, jv);
     const IO* p = x + off + s.s0 * step;
     const IO* q = dy + off + s.s0 * step;
-#pragma unroll 2
-    for (int64_t t = s.s0; t < s.s1; ++t) {
-      push<K>(xw, jv ? load_wide(p) : 0.0);
+    float* dm = dhm ? dhm + off + s.s0 * step : nullptr;  // materialised dh2 | h1 - mu for bwd_dx_mat
+    stream_any<(K > 8 ? 4 : 8), true>(ring, ct, p, q, x, dy, step, s.s0, s.s1, s.s1, [&](IO xv, IO dv, int64_t, int64_t eo) {
+      const double v = wide(xv);
+      push<K>(xw, v);
+      xsum += v;
       const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
       const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps<K>(wq, xw), bf));
-      const double dh2 = jv ? dh2_of<IO>(sur, skind, alpha, h2, q) : 0.0;
+      const double dh2 = jv ? dh2_val<IO>(sur, skind, alpha, h2, dv) : 0.0;
       const double hc = h1 - mu;
+      if (dm && jv) {
+        dm[eo] = (float)dh2;
+        dm[nel + eo] = (float)hc;
+      }
       db += dh2;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         dwq[i] = fma(xw[i], dh2, dwq[i]);
-        sx[i] += xw[i];
         sxc[i] = fma(xw[i], hc, sxc[i]);
       }
-      p += step;
-      q += step;
+    });
+    if (s.s1 == s.Sr) {
+      double run = 0.0;
+#pragma unroll
+      for (int i = K - 2; i >= 0; --i) {
+        run += xw[i + 1];
+        tails[i][warp][lane] += run;
+      }
     }
   }
   // block reduction over warps in fixed order, 8 values per round
@@ -502,7 +540,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         if (v == 1 + i) val = dwq[i];
-        if (v == 1 + K + i) val = sx[i];
+        if (v == 1 + K + i) val = (i < K - 1) ? xsum - tails[i < K - 1 ? i : 0][warp][lane] : xsum;
         if (v == 1 + 2 * K + i) val = sxc[i];
       }
       sh[warp][u][lane] = val;
@@ -521,8 +559,10 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
   }
 }
 
-// backward fold: one warp per channel; writes dW (per channel into dwtmp when
-// shared), dgamma, dbeta and the BN-through-stats scalars (alpha1, beta1).
+// backward fold: one block per channel, each warp sums some of the 3K+1
+// values over the partial rows (lanes over rows, fixed-order shuffle tree),
+// then one thread writes dW (per channel into dwtmp when shared), dgamma,
+// dbeta and the BN-through-stats scalars (alpha1, beta1).
 __global__ void __launch_bounds__(kThreads) bwd_fold_kernel(Geom g, const double* __restrict__ part,
                                                             const double* __restrict__ W, int flags,
                                                             const double* __restrict__ gamma,
@@ -531,14 +571,13 @@ __global__ void __launch_bounds__(kThreads) bwd_fold_kernel(Geom g, const double
                                                             double* __restrict__ dgamma,
                                                             double* __restrict__ dbeta,
                                                             double* __restrict__ bfold) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (c >= g.C) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x;
   const int K = g.k;
   const int NV = 3 * K + 1;
-  double tot[3 * PSN_MAX_ORDER + 1];
+  __shared__ double tot[3 * PSN_MAX_ORDER + 1];
   const int64_t total = g.rows * g.Q;
-  for (int v = 0; v < NV; ++v) {
+  for (int v = warp; v < NV; v += kWarps) {
     double acc = 0.0;
     for (int64_t idx = lane; idx < total; idx += 32) {
       const int64_t r = idx / g.Q, q = idx % g.Q;
@@ -549,9 +588,10 @@ __global__ void __launch_bounds__(kThreads) bwd_fold_kernel(Geom g, const double
       const double o = __shfl_xor_sync(0xffffffffu, acc, off);
       acc = (lane & off) ? o + acc : acc + o;
     }
-    tot[v] = acc;
+    if (lane == 0) tot[v] = acc;
   }
-  if (lane != 0) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   const double* f = fold + c * PSN_FOLD_STRIDE(K);
   const double mu = f[0], s = f[1], a = f[2];
   const bool quantized = (flags & PSN_QUANTIZED) &&
@@ -631,6 +671,9 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
   const double alpha1 = jv ? bfold[2 * c] : 0.0;
   const double beta1 = jv ? bfold[2 * c + 1] : 0.0;
   const int64_t step = (int64_t)g.d * g.row;
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  IO* ring = reinterpret_cast<IO*>(psn_dsm) + warp * 2 * kRingSteps * 32;
+  const ColTile ct = col_tile<IO>(g, x, dy);
   for (int64_t seg = (int64_t)blockIdx.y * kWarps + warp; seg < g.nseg;
        seg += (int64_t)gridDim.y * kWarps) {
     Seg s;
@@ -645,13 +688,14 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
     const IO* q = dy + off + s.s0 * step;
     IO* o = dx + off + (s.s0 - (K - 1)) * step;
     const int64_t tend = s.s1 + K - 1;
-    for (int64_t t = s.s0; t < tend; ++t) {
+    const int64_t lim = tend < s.Sr ? tend : s.Sr;
+    stream_any<(K > 8 ? 4 : 8), true>(ring, ct, p, q, x, dy, step, s.s0, tend, lim, [&](IO xv, IO dv, int64_t t, int64_t eo) {
       Acc dh2 = (Acc)0, dh1 = (Acc)0;
       if (t < s.Sr) {
-        push<K>(xw, jv ? load_wide(p) : 0.0);
+        push<K>(xw, wide(xv));
         const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
         const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps<K>(wq, xw), bf));
-        dh2 = jv ? (Acc)dh2_of<IO>(sur, skind, alpha, h2, q) : (Acc)0;
+        dh2 = jv ? (Acc)dh2_val<IO>(sur, skind, alpha, h2, dv) : (Acc)0;
         dh1 = (Acc)(alpha1 + beta1 * (h1 - mu));
       }
 #pragma unroll
@@ -659,20 +703,81 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
         pacc[i] = fma(wqa[i], dh2, pacc[i]);
         pacc[i] = fma(wa[i], dh1, pacc[i]);
       }
-      if (t - (K - 1) >= s.s0 && jv) Carrier<IO>::store(o, (double)pacc[0]);
+      if (t - (K - 1) >= s.s0 && jv) Carrier<IO>::store(o + eo, (double)pacc[0]);
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) pacc[i] = pacc[i + 1];
       pacc[K - 1] = (Acc)0;
-      p += step;
-      q += step;
-      o += step;
-    }
+    });
+  }
+}
+
+// backward pass 2 from dh2 and h1 - mu materialised (f32) by bwd_reduce:
+// dx[t] = sum_i w_q,i dh2[t+off_i] + W_i dh1[t+off_i], dh1 = alpha1 + beta1 (h1 - mu),
+// FP32 only (the recomputing bwd_dx_kernel spends 2k DFMA per element on h1, h2)
+template <int K, typename IO>
+__global__ void __launch_bounds__(kThreads, 2) bwd_dx_mat_kernel(Geom g, const float* __restrict__ dhm,
+                                                                 const double* __restrict__ W, int shared,
+                                                                 const double* __restrict__ fold,
+                                                                 const double* __restrict__ bfold,
+                                                                 IO* __restrict__ dx) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const bool jv = j < g.J;
+  const int64_t c = jv ? j / g.Q : 0;
+  const double* f = fold + c * PSN_FOLD_STRIDE(K);
+  float wa[K], wqa[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    wa[i] = jv ? (float)W[(shared ? 0 : c) * K + i] : 0.0f;
+    wqa[i] = jv ? (float)f[PSN_FOLD_HDR + K + i] : 0.0f;
+  }
+  const float a1 = jv ? (float)bfold[2 * c] : 0.0f;
+  const float b1 = jv ? (float)bfold[2 * c + 1] : 0.0f;
+  const int64_t step = (int64_t)g.d * g.row;
+  const int64_t nel = g.T * g.row;
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  float* ring = reinterpret_cast<float*>(psn_dsm) + warp * 2 * kRingSteps * 32;
+  const ColTile ct = col_tile<float>(g, dhm, dhm + nel);
+  for (int64_t seg = (int64_t)blockIdx.y * kWarps + warp; seg < g.nseg;
+       seg += (int64_t)gridDim.y * kWarps) {
+    Seg s;
+    if (!decode_seg(g, seg, s)) continue;
+    const int64_t off = (int64_t)s.r * g.row + s.n * g.J + j;
+    float pacc[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) pacc[i] = 0.0f;
+    const float* p = dhm + off + s.s0 * step;
+    IO* o = dx + off + (s.s0 - (K - 1)) * step;
+    const int64_t tend = s.s1 + K - 1;
+    const int64_t lim = tend < s.Sr ? tend : s.Sr;
+    stream_any<8, true>(ring, ct, p, p + nel, dhm, dhm, step, s.s0, tend, lim,
+                     [&](float d2, float hc, int64_t t, int64_t eo) {
+      const float dh1 = (t < s.Sr) ? fmaf(b1, hc, a1) : 0.0f;  // d2 reads 0 there
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        pacc[i] = fmaf(wqa[i], d2, pacc[i]);
+        pacc[i] = fmaf(wa[i], dh1, pacc[i]);
+      }
+      if (t - (K - 1) >= s.s0 && jv) Carrier<IO>::storef(o + eo, pacc[0]);
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i) pacc[i] = pacc[i + 1];
+      pacc[K - 1] = 0.0f;
+    });
   }
 }
 
 // ------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------
+// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
+template <typename Kern>
+int smem_optin(Kern* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return PSN_OK;
+  if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (generic kernel smem) failed");
+  return PSN_OK;
+}
 inline dim3 grid_red(const Geom& g) { return dim3((unsigned)g.ctiles, (unsigned)g.rows); }
 inline dim3 grid_map(const Geom& g) {
   int64_t y = (g.nseg + kWarps - 1) / kWarps;
@@ -686,15 +791,20 @@ int launch_forward(const psn_desc_t* desc, const Geom& g, const void* x, const d
                    double* fold, char* ws, const WsLayout& L, cudaStream_t st) {
   double* part1 = (double*)(ws + L.part1);
   const int shared = (desc->flags & PSN_SHARED) ? 1 : 0;
-  fwd_stats_kernel<K, IO><<<grid_red(g), kThreads, 0, st>>>(g, (const IO*)x, W, shared, part1);
+  const size_t sm1 = ring_bytes<IO>(1);
+  int rc;
+  if ((rc = smem_optin(fwd_stats_kernel<K, IO>, sm1)) || (rc = smem_optin(fwd_spike_kernel<K, IO, 0>, sm1)) ||
+      (rc = smem_optin(fwd_spike_kernel<K, IO, 1>, sm1)))
+    return rc;
+  fwd_stats_kernel<K, IO><<<grid_red(g), kThreads, sm1, st>>>(g, (const IO*)x, W, shared, part1);
   fwd_fold_kernel<<<(unsigned)((g.C + kWarps - 1) / kWarps), kThreads, 0, st>>>(
       g, part1, W, desc->flags, gamma, beta, rm, rv, desc->eps, desc->momentum, fold);
   if (desc->flags & PSN_SMOOTH)
-    fwd_spike_kernel<K, IO, 1><<<grid_map(g), kThreads, 0, st>>>(g, (const IO*)x, fold, desc->surrogate,
-                                                                   desc->alpha, (IO*)out);
+    fwd_spike_kernel<K, IO, 1><<<grid_map(g), kThreads, sm1, st>>>(g, (const IO*)x, fold, desc->surrogate,
+                                                                     desc->alpha, (IO*)out);
   else
-    fwd_spike_kernel<K, IO, 0><<<grid_map(g), kThreads, 0, st>>>(g, (const IO*)x, fold, desc->surrogate,
-                                                                   desc->alpha, (IO*)out);
+    fwd_spike_kernel<K, IO, 0><<<grid_map(g), kThreads, sm1, st>>>(g, (const IO*)x, fold, desc->surrogate,
+                                                                     desc->alpha, (IO*)out);
   return cuda_check("psn_forward_train");
 }
 
@@ -707,13 +817,22 @@ int launch_backward(const psn_desc_t* desc, const Geom& g, const void* x, const 
   double* dwtmp = (double*)(ws + L.dwtmp);
   const int shared = (desc->flags & PSN_SHARED) ? 1 : 0;
   const Surrogate sur = make_surrogate(desc);
-  bwd_reduce_kernel<K, IO><<<grid_red(g), kThreads, 0, st>>>(g, (const IO*)x, (const IO*)dy, W, shared, fold,
-                                                             sur, desc->surrogate, desc->alpha, part3);
-  bwd_fold_kernel<<<(unsigned)((g.C + kWarps - 1) / kWarps), kThreads, 0, st>>>(
+  float* dhm = L.dhm_bytes ? (float*)(ws + L.dhm) : nullptr;
+  const size_t sm2 = ring_bytes<IO>(2), smf = ring_bytes<float>(2);
+  int rc;
+  if ((rc = smem_optin(bwd_reduce_kernel<K, IO>, sm2)) || (rc = smem_optin(bwd_dx_kernel<K, IO>, sm2)) ||
+      (rc = smem_optin(bwd_dx_mat_kernel<K, IO>, smf)))
+    return rc;
+  bwd_reduce_kernel<K, IO><<<grid_red(g), kThreads, sm2, st>>>(g, (const IO*)x, (const IO*)dy, W, shared, fold,
+                                                               sur, desc->surrogate, desc->alpha, part3, dhm);
+  bwd_fold_kernel<<<(unsigned)g.C, kThreads, 0, st>>>(
       g, part3, W, desc->flags, gamma, fold, shared ? dwtmp : dW, dgamma, dbeta, bfold);
   if (shared) shared_rowsum_kernel<<<1, 32, 0, st>>>(dwtmp, g.C, K, dW);
-  bwd_dx_kernel<K, IO><<<grid_map(g), kThreads, 0, st>>>(g, (const IO*)x, (const IO*)dy, W, shared, fold,
-                                                         bfold, sur, desc->surrogate, desc->alpha, (IO*)dx);
+  if (dhm)
+    bwd_dx_mat_kernel<K, IO><<<grid_map(g), kThreads, smf, st>>>(g, dhm, W, shared, fold, bfold, (IO*)dx);
+  else
+    bwd_dx_kernel<K, IO><<<grid_map(g), kThreads, sm2, st>>>(g, (const IO*)x, (const IO*)dy, W, shared, fold,
+                                                             bfold, sur, desc->surrogate, desc->alpha, (IO*)dx);
   return cuda_check("psn_backward");
 }
 
@@ -723,8 +842,10 @@ int launch_eval(const psn_desc_t* desc, const Geom& g, const void* x, const doub
                 void* out, double* fold, cudaStream_t st) {
   eval_fold_kernel<<<(unsigned)((g.C + 127) / 128), 128, 0, st>>>(g, W, desc->flags, gamma, beta, rm, rv,
                                                                    desc->eps, fold);
-  fwd_spike_kernel<K, IO, 2><<<grid_map(g), kThreads, 0, st>>>(g, (const IO*)x, fold, desc->surrogate,
-                                                                 desc->alpha, (IO*)out);
+  const size_t sm1 = ring_bytes<IO>(1);
+  if (int rc = smem_optin(fwd_spike_kernel<K, IO, 2>, sm1)) return rc;
+  fwd_spike_kernel<K, IO, 2><<<grid_map(g), kThreads, sm1, st>>>(g, (const IO*)x, fold, desc->surrogate,
+                                                                   desc->alpha, (IO*)out);
   return cuda_check("psn_forward_eval");
 }
 

@@ -70,6 +70,11 @@ static unsigned long long wait_limit_ns() {
 
 bool eligible(const psn_desc_t* desc) {
   if (env_int("PSN_FORCE_GENERIC", 0)) return false;
+  return shape_eligible(desc);
+}
+
+bool shape_eligible(const psn_desc_t* desc) {
+  if (desc->flags & PSN_GENERIC) return false;
   if (desc->dtype != PSN_F32 && desc->dtype != PSN_BF16) return false;
   if (desc->k > 8 || desc->d > 3) return false;   // instantiated orders / sawtooth dilations
   // spatial inputs (Q > 1): the per-channel sums of a group are merged from its

@@ -310,13 +310,6 @@ __device__ __forceinline__ double round_f32_sg(double h) {
   return __longlong_as_double((long long)r);
 }
 
-// 1/v to ~2^-44 relative: MUFU.RCP64H seed (~2^-22) and one Newton step
-__device__ __forceinline__ double rcp_f64(double v) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
-  const double e = fma(-v, r, 1.0);
-  return fma(r, e, r);
-}
 
 // -------------------------------------------------------------------------
 // shared-memory layout per (order, dilation, carrier size, direction); host

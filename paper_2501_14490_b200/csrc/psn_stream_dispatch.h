@@ -11,7 +11,8 @@ int run_f32_bwd(int k, int d, const Args& a, const void* x, const void* dy, cuda
 int run_bf16_fwd(int k, int d, const Args& a, const void* x, const void* dy, cudaStream_t st);
 int run_bf16_bwd(int k, int d, const Args& a, const void* x, const void* dy, cudaStream_t st);
 
-bool eligible(const psn_desc_t* desc);
+bool eligible(const psn_desc_t* desc);        // shape_eligible and not PSN_FORCE_GENERIC
+bool shape_eligible(const psn_desc_t* desc);  // the shape / carrier alone (no run-time knobs)
 bool aligned_for_tma(const void* x, const void* dy);
 bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p);
 size_t workspace_bytes(const psn_desc_t* desc);

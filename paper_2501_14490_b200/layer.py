@@ -44,11 +44,12 @@ class Mode(Enum):
 
 @dataclass(frozen=True)
 class LayerMethod:
-    """One implementation choice of a layer (network.py:58-64).  Here there is
-    one fused kernel family; the planner picks the streamed persistent kernels
-    or the generic three-launch kernels from the shape, so the only candidate
-    is "stream" (the reference's engine registry is a CPU stand-in for GPU
-    methods, out of scope: SURVEY.md section 2)."""
+    """One implementation choice of a layer (network.py:58-64): "stream" lets
+    the planner pick the streamed persistent kernels or the generic
+    three-launch kernels from the shape; "generic" always takes the
+    three-launch kernels (descriptor flag PSN_GENERIC).  The reference's
+    engine registry is a CPU stand-in for GPU methods, out of scope
+    (SURVEY.md section 2)."""
 
     name: str = "stream"
     engine: object = None
@@ -131,11 +132,11 @@ class SpikingLayer(nn.Module):
         return [self.W, self.gamma, self.beta]
 
     def method_candidates(self, layout=None) -> list:
-        return [LayerMethod("stream")]
+        return [LayerMethod("stream"), LayerMethod("generic")]
 
     def configure(self, method: LayerMethod) -> None:
-        if method.name != "stream":
-            raise ValueError(f"unknown layer method {method.name!r} (the fused kernels are the only method)")
+        if method.name not in ("stream", "generic"):
+            raise ValueError(f"unknown layer method {method.name!r} (the fused kernels: 'stream' or 'generic')")
         self.method = method
 
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
@@ -178,6 +179,8 @@ class SpikingLayer(nn.Module):
             f |= L.PSN_QUANTIZE_IN_SMOOTH
         if self.cfg.grad_mode is QuantGradMode.ROUND_STE:
             f |= L.PSN_ROUND_STE
+        if self.method.name == "generic":
+            f |= L.PSN_GENERIC
         return f
 
     def _desc_args(self, mode: Mode):

@@ -46,12 +46,14 @@ def _layer_from_fixture(meta, z):
     return layer
 
 
+@pytest.mark.parametrize("method", ["stream", "generic"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_layer_matches_reference_fixture(name):
+def test_layer_matches_reference_fixture(name, method):
     P = _P()
     meta = CASES[name]
     z = np.load(os.path.join(GOLDEN, f"layer_{name}.npz"))
     layer = _layer_from_fixture(meta, z)
+    layer.configure(P.layer.LayerMethod(method))
     smooth = meta["mode"] == "smooth"
     mode = P.Mode.SMOOTH if smooth else P.Mode.TRAIN
     f64 = meta["dtype"] == "float64"
@@ -99,7 +101,8 @@ def test_layer_matches_reference_fixture(name):
     spikes_match_except_ties(got, z["eval_out"], z["eval_x"].astype(np.float32), w, b, d, "eval spikes")
 
 
-def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0, spatial=(), x_fn=None):
+def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0, spatial=(), x_fn=None,
+                         method="stream"):
     """Full-size GPU fwd+bwd; oracle on a channel subset (exact restatement:
     channels are independent in forward and backward).  `spatial` adds axes
     after C (rank 4/5, the reference's [T, N, C, H, W]); `x_fn(rng, shape)`
@@ -111,6 +114,7 @@ def _oracle_subset_check(T, N, C, k, d, channels, dtype=torch.float32, seed=0, s
     dy_np = rng.standard_normal(shape).astype(np.float32)
     cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
     layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(seed + 1), device="cuda")
+    layer.configure(P.layer.LayerMethod(method))
     x = torch.tensor(x_np, device="cuda", dtype=dtype, requires_grad=True)
     out = layer(x, P.Mode.TRAIN)
     out.backward(torch.tensor(dy_np, device="cuda", dtype=dtype))
@@ -149,6 +153,29 @@ def test_metric_config_parity_on_channel_subset(d):
     """T=1024, B=64, C=512, k=4 (BASELINE metric config), sawtooth d."""
     flips = _oracle_subset_check(1024, 64, 512, 4, d, channels=[0, 1, 77, 255, 256, 400, 510, 511], seed=d)
     assert flips <= 2
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_metric_config_parity_generic_method(d):
+    """The metric config through the generic three-launch kernels (descriptor
+    flag PSN_GENERIC: the shared-memory-ring streaming loops and the
+    materialised dh2 / h1 - mu backward)."""
+    flips = _oracle_subset_check(1024, 64, 512, 4, d, channels=list(range(0, 512, 4)), seed=200 + d,
+                                 method="generic")
+    assert flips <= 4
+
+
+@pytest.mark.parametrize("shape,k,d,dt,off", [
+    ((250, 32, 128), 4, 1, torch.float32, 0.0),     # config 1
+    ((300, 7, 45), 16, 3, torch.float32, 50.0),     # ragged tile (J % 4 != 0: scalar copies), offset mean
+    ((64, 5, 12, 3, 3), 6, 2, torch.float32, 0.0),  # spatial, k > 4
+    ((200, 9, 96), 8, 3, torch.bfloat16, 0.0),      # bf16: register prefetch
+])
+def test_generic_method_parity(shape, k, d, dt, off):
+    T, N, C = shape[:3]
+    flips = _oracle_subset_check(T, N, C, k, d, channels=list(range(C)), dtype=dt, seed=7, spatial=shape[3:],
+                                 x_fn=lambda rng, sh: rng.standard_normal(sh) + off, method="generic")
+    assert flips <= 4
 
 
 @pytest.mark.parametrize("d", [1, 2, 3])

@@ -208,7 +208,7 @@ def test_explicit_layer_backward_matches_autograd():
         assert torch.equal(pa.grad, pb.grad)
     b.backward(dy)  # accumulates like the reference's +=
     assert torch.equal(b.W.grad, 2 * a.W.grad)
-    assert [m.name for m in b.method_candidates()] == ["stream"]
+    assert [m.name for m in b.method_candidates()] == ["stream", "generic"]
     with pytest.raises(ValueError):
         b.configure(P.layer.LayerMethod("matmul"))
 
