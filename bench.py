@@ -203,7 +203,7 @@ class Workload:
     """One rank's share of the neuron layer step, driven through the C ABI:
     spikes/dx and a GradBucket whose views receive dW, dgamma, dbeta."""
 
-    def __init__(self, P, L, dev, shape, k, d, dt, seed, use_graph):
+    def __init__(self, P, L, dev, shape, k, d, dt, seed, use_graph, extra_flags=0):
         import numpy as np
         import torch
         from paper_2501_14490_b200 import ddp
@@ -218,7 +218,7 @@ class Workload:
         self.dy = torch.randn(shape, generator=g, device=dev).to(dt)
         cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
         self.layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(1), device=dev)
-        flags = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
+        flags = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS | extra_flags
         self.desc = L.make_desc(self.x.shape, k, d, dt, flags=flags)
         self.ws = L.workspace(self.desc, dev)
         self.out = torch.empty_like(self.x)

@@ -70,9 +70,12 @@ typedef enum {
   PSN_SMOOTH = 8,                  /* Mode.SMOOTH: primitive output, stats frozen  */
   PSN_QUANTIZE_IN_SMOOTH = 16,     /* SpikingLayer.quantize_in_smooth_mode         */
   PSN_ROUND_STE = 32,              /* QuantGradMode.ROUND_STE (else WHOLE_STE)     */
-  PSN_GENERIC = 64                 /* force the three-launch kernels (no streamed  */
+  PSN_GENERIC = 64,                /* force the three-launch kernels (no streamed  */
                                    /* kernel); part of the descriptor so that the  */
                                    /* workspace size and the call agree            */
+  PSN_STREAM = 128                 /* streamed kernels whenever the shape allows   */
+                                   /* them (skip the small-size / wide-window      */
+                                   /* preference for the three-launch kernels)     */
 } psn_flag_t;
 
 typedef struct {

@@ -27,6 +27,7 @@ PSN_SMOOTH = 8
 PSN_QUANTIZE_IN_SMOOTH = 16
 PSN_ROUND_STE = 32
 PSN_GENERIC = 64
+PSN_STREAM = 128
 PSN_FOLD_HDR = 7
 
 

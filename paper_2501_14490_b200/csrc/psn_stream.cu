@@ -73,8 +73,22 @@ bool eligible(const psn_desc_t* desc) {
   return shape_eligible(desc);
 }
 
+// Routing between the streamed kernel and the three generic launches, measured
+// on B200 (profiles/r2_route.txt, CUDA-graph replay of fwd+bwd): below ~1.5M
+// elements the streamed kernel's cross-CTA synchronisation skeleton costs more
+// than the whole generic pass (BASELINE config 1, 1.0M elements: 0.049 vs
+// 0.039 ms), and the widest windows ((k-1) d > 16: k = 8, d = 3) spill
+// registers in the streamed kernels (0.73 vs 0.53 ms).  PSN_STREAM in the
+// descriptor skips this preference.
+bool prefer_generic(const psn_desc_t* desc) {
+  if (desc->flags & PSN_STREAM) return false;
+  if ((double)desc->T * desc->N * desc->C * desc->Q < 1.5e6) return true;
+  return (desc->k - 1) * desc->d > 16;
+}
+
 bool shape_eligible(const psn_desc_t* desc) {
   if (desc->flags & PSN_GENERIC) return false;
+  if (prefer_generic(desc)) return false;
   if (desc->dtype != PSN_F32 && desc->dtype != PSN_BF16) return false;
   if (desc->k > 8 || desc->d > 3) return false;   // instantiated orders / sawtooth dilations
   // spatial inputs (Q > 1): the per-channel sums of a group are merged from its
@@ -88,8 +102,10 @@ bool shape_eligible(const psn_desc_t* desc) {
   return true;
 }
 
-bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p) {
-  if (!eligible(desc)) return false;
+bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p, bool for_sizing) {
+  // workspace sizing ignores PSN_FORCE_GENERIC: a workspace sized while the
+  // knob was set must still fit a later streamed call
+  if (!(for_sizing ? shape_eligible(desc) : eligible(desc))) return false;
   const DevAttr* da = dev_attr();
   if (!da || !g_encode || da->sms <= 0 || !da->coop) return false;
   const int g_sms = da->sms, g_smem_optin = da->smem_optin;
@@ -180,7 +196,7 @@ size_t workspace_bytes(const psn_desc_t* desc) {
   size_t need = 0;
   for (int b = 0; b < 2; ++b) {
     Plan p;
-    if (!make_plan(desc, b == 1, p)) continue;
+    if (!make_plan(desc, b == 1, p, true)) continue;
     const size_t bytes = a256(zeroed_bytes(p, b == 1));
     if (bytes > need) need = bytes;
   }

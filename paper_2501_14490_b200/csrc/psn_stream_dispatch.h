@@ -14,7 +14,7 @@ int run_bf16_bwd(int k, int d, const Args& a, const void* x, const void* dy, cud
 bool eligible(const psn_desc_t* desc);        // shape_eligible and not PSN_FORCE_GENERIC
 bool shape_eligible(const psn_desc_t* desc);  // the shape / carrier alone (no run-time knobs)
 bool aligned_for_tma(const void* x, const void* dy);
-bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p);
+bool make_plan(const psn_desc_t* desc, bool bwd, Plan& p, bool for_sizing = false);
 size_t workspace_bytes(const psn_desc_t* desc);
 int forward(const psn_desc_t* desc, const Plan& p, const void* x, const double* W, const double* gamma,
             const double* beta, double* rm, double* rv, void* out, double* fold, void* ws, cudaStream_t st);

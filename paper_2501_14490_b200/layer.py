@@ -44,14 +44,15 @@ class Mode(Enum):
 
 @dataclass(frozen=True)
 class LayerMethod:
-    """One implementation choice of a layer (network.py:58-64): "stream" lets
+    """One implementation choice of a layer (network.py:58-64): "auto" lets
     the planner pick the streamed persistent kernels or the generic
-    three-launch kernels from the shape; "generic" always takes the
-    three-launch kernels (descriptor flag PSN_GENERIC).  The reference's
-    engine registry is a CPU stand-in for GPU methods, out of scope
-    (SURVEY.md section 2)."""
+    three-launch kernels from the shape (small or widest-window shapes take
+    the generic ones); "stream" takes the streamed kernels whenever the shape
+    allows (descriptor flag PSN_STREAM); "generic" always takes the
+    three-launch kernels (PSN_GENERIC).  The reference's engine registry is a
+    CPU stand-in for GPU methods, out of scope."""
 
-    name: str = "stream"
+    name: str = "auto"
     engine: object = None
     block_size: int | None = None
 
@@ -121,7 +122,7 @@ class SpikingLayer(nn.Module):
         self.quantize_in_smooth_mode = False
         self.last_fold = None
         self._last = None
-        self.method = LayerMethod("stream")
+        self.method = LayerMethod("auto")
 
     # -- reference-compatible helpers (network.py:162-209) ----------------------
     def out_channels(self) -> int:
@@ -132,11 +133,11 @@ class SpikingLayer(nn.Module):
         return [self.W, self.gamma, self.beta]
 
     def method_candidates(self, layout=None) -> list:
-        return [LayerMethod("stream"), LayerMethod("generic")]
+        return [LayerMethod("auto"), LayerMethod("stream"), LayerMethod("generic")]
 
     def configure(self, method: LayerMethod) -> None:
-        if method.name not in ("stream", "generic"):
-            raise ValueError(f"unknown layer method {method.name!r} (the fused kernels: 'stream' or 'generic')")
+        if method.name not in ("auto", "stream", "generic"):
+            raise ValueError(f"unknown layer method {method.name!r} ('auto', 'stream' or 'generic')")
         self.method = method
 
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
@@ -181,6 +182,8 @@ class SpikingLayer(nn.Module):
             f |= L.PSN_ROUND_STE
         if self.method.name == "generic":
             f |= L.PSN_GENERIC
+        elif self.method.name == "stream":
+            f |= L.PSN_STREAM
         return f
 
     def _desc_args(self, mode: Mode):

@@ -155,6 +155,20 @@ def test_metric_config_parity_on_channel_subset(d):
     assert flips <= 2
 
 
+def test_routing_rule():
+    """The planner's choice (PSN_STREAM / PSN_GENERIC unset): BASELINE config 1
+    (1.0M elements) and k = 8, d = 3 on the generic kernels, the metric shape
+    and the 8-GPU shard on the streamed ones; PSN_STREAM overrides."""
+    from paper_2501_14490_b200 import _lib as L
+    base = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
+    for shape, k, d, want in [((250, 32, 128), 4, 1, 0), ((1024, 64, 512), 8, 3, 0), ((1024, 64, 512), 4, 1, 1),
+                              ((1024, 8, 512), 4, 3, 1), ((1024, 64, 512), 6, 3, 1)]:
+        for bwd in (False, True):
+            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base), bwd)["streamed"] == want, shape
+            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base | L.PSN_STREAM), bwd)["streamed"] == 1
+            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base | L.PSN_GENERIC), bwd)["streamed"] == 0
+
+
 @pytest.mark.parametrize("d", [1, 2, 3])
 def test_metric_config_parity_generic_method(d):
     """The metric config through the generic three-launch kernels (descriptor
@@ -232,11 +246,11 @@ def test_spatial_inputs_streamed_parity(shape, k, d, dt):
     span several 32-column tiles and the per-channel sums merge the column sums
     (segmented warp scan); every channel against the oracle."""
     from paper_2501_14490_b200 import _lib as L
-    desc = L.make_desc(shape, k, d, dt, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+    desc = L.make_desc(shape, k, d, dt, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS | L.PSN_STREAM)
     assert L.plan_info(desc, False)["streamed"] == 1 and L.plan_info(desc, True)["streamed"] == 1
     T, N, C = shape[:3]
     _oracle_subset_check(T, N, C, k, d, channels=list(range(C)), dtype=dt, seed=sum(shape) + k,
-                         spatial=shape[3:])
+                         spatial=shape[3:], method="stream")
 
 
 FLAG_CASES = [
@@ -253,12 +267,14 @@ FLAG_CASES = [
 ]
 
 
+@pytest.mark.parametrize("method", ["stream", "generic"])
 @pytest.mark.parametrize("name,shape,k,d,flags", FLAG_CASES, ids=[c[0] for c in FLAG_CASES])
-def test_streamed_flag_matrix_two_steps(name, shape, k, d, flags):
-    """The streamed kernels under every layer option the reference has (shared
-    weights, ROUND_STE, rational surrogate, float weights, running-stat fusion),
-    orders 3-8, T and N off the tile grid, random gamma / beta / running stats;
-    two steps, so the second uses the running statistics the first updated."""
+def test_flag_matrix_two_steps(name, shape, k, d, flags, method):
+    """The streamed and the generic kernels under every layer option the
+    reference has (shared weights, ROUND_STE, rational surrogate, float
+    weights, running-stat fusion), orders 3-8, T and N off the tile grid,
+    random gamma / beta / running stats; two steps, so the second uses the
+    running statistics the first updated."""
     P = _P()
     from paper_2501_14490_b200 import _lib as L
     T, N, C = shape
@@ -269,6 +285,7 @@ def test_streamed_flag_matrix_two_steps(name, shape, k, d, flags):
     sur = P.SurrogateConfig(P.SurrogateKind(flags.get("surrogate", "arctan")), flags.get("alpha", 2.0))
     layer = P.SpikingLayer(cfg, surrogate=sur, weight_init="uniform", rng=np.random.default_rng(7), device="cuda",
                            fuse_from_batch_stats=flags.get("fuse_from_batch_stats", True))
+    layer.configure(P.layer.LayerMethod(method))
     gamma, beta = rng.uniform(0.5, 1.5, C), rng.uniform(-1.5, 0.5, C)
     rm, rv = rng.normal(0.0, 0.3, C), rng.uniform(0.5, 2.0, C)
     with torch.no_grad():
@@ -277,7 +294,8 @@ def test_streamed_flag_matrix_two_steps(name, shape, k, d, flags):
         layer.running_mean.copy_(torch.from_numpy(rm))
         layer.running_var.copy_(torch.from_numpy(rv))
     desc = L.make_desc(shape, k, d, torch.float32, flags=layer._flags(P.Mode.TRAIN))
-    assert L.plan_info(desc, False)["streamed"] == 1 and L.plan_info(desc, True)["streamed"] == 1
+    want = 1 if method == "stream" else 0
+    assert L.plan_info(desc, False)["streamed"] == want and L.plan_info(desc, True)["streamed"] == want
     p = O.init_layer(C, k, d, weight_init="uniform", rng=np.random.default_rng(7), shared=flags.get("shared", False),
                      quantized=flags.get("quantized", True), round_ste=flags.get("round_ste", False),
                      fuse_from_batch_stats=flags.get("fuse_from_batch_stats", True),
@@ -373,8 +391,9 @@ def test_input_validation_errors():
         layer(torch.randn(5, 2, 4), P.Mode.TRAIN)  # CPU tensor: no CPU fallback
 
 
+@pytest.mark.parametrize("method", ["stream", "generic"])
 @pytest.mark.parametrize("k,d", [(4, 2), (3, 1)])
-def test_exact_threshold_ties_are_bit_exact(k, d):
+def test_exact_threshold_ties_are_bit_exact(k, d, method):
     """Membranes exactly at / next to the threshold: integer inputs, running-stat
     fusion (b_f = beta exactly) and beta in {0, +-1e-45, -1e-46}.  The streamed
     forward decides spikes with an f32 filter and falls back to the exact f64
@@ -389,6 +408,7 @@ def test_exact_threshold_ties_are_bit_exact(k, d):
     cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
     layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(k), device="cuda",
                            fuse_from_batch_stats=False)
+    layer.configure(P.layer.LayerMethod(method))
     betas = np.array([0.0, -1e-45, -1e-46, 1e-45, 0.25, -0.25, 0.0, -1e-45] * (C // 8))
     with torch.no_grad():
         layer.beta.copy_(torch.tensor(betas, dtype=torch.float64))
@@ -414,7 +434,8 @@ def test_cta_teams_and_lag_parity(monkeypatch, teams, lag):
     results as the reference."""
     monkeypatch.setenv("PSN_TEAMS", str(teams))
     monkeypatch.setenv("PSN_LAG", str(lag))
-    _oracle_subset_check(400, 24, 320, 4, 2, channels=[0, 33, 97, 160, 255, 319], seed=teams * 10 + lag)
+    _oracle_subset_check(400, 24, 320, 4, 2, channels=[0, 33, 97, 160, 255, 319], seed=teams * 10 + lag,
+                         method="stream")
 
 
 def _abi_step(P, L, x, dy, layer, desc, ws):
@@ -438,10 +459,12 @@ def _abi_step(P, L, x, dy, layer, desc, ws):
     return [t.cpu() for t in (out, dx, dW, dg, db, rm, rv)]
 
 
-def test_workspace_reuse_garbage_and_alternating_geometries():
+@pytest.mark.parametrize("route", ["stream", "auto"])
+def test_workspace_reuse_garbage_and_alternating_geometries(route):
     """Workspace contract: any content is fine.  Repeated calls, a garbage-filled
     buffer and a buffer alternating between two geometries must all give the
-    same results as a fresh zeroed workspace."""
+    same results as a fresh zeroed workspace (streamed kernels, and the
+    planner's choice at these sizes: the generic ones)."""
     P = _P()
     from paper_2501_14490_b200 import _lib as L
     shapes = [(300, 20, 128), (257, 12, 64)]
@@ -451,7 +474,9 @@ def test_workspace_reuse_garbage_and_alternating_geometries():
         layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(C), device="cuda")
         x = torch.randn((T, N, C), device="cuda")
         dy = torch.randn((T, N, C), device="cuda")
-        desc = L.make_desc(x.shape, 4, 2, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+        extra = L.PSN_STREAM if route == "stream" else 0
+        desc = L.make_desc(x.shape, 4, 2, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS | extra)
+        assert L.plan_info(desc, True)["streamed"] == (1 if route == "stream" else 0)
         runs.append((x, dy, layer, desc))
     nbytes = max(int(L.lib().psn_workspace_bytes(__import__("ctypes").byref(r[3]))) for r in runs)
     refs = [_abi_step(P, L, x, dy, layer, desc, torch.zeros(nbytes, dtype=torch.uint8, device="cuda"))
@@ -467,7 +492,8 @@ def test_workspace_reuse_garbage_and_alternating_geometries():
             same(_abi_step(P, L, x, dy, layer, desc, shared), ref)
 
 
-def test_cuda_graph_capture_replays_the_step():
+@pytest.mark.parametrize("route", ["stream", "auto"])
+def test_cuda_graph_capture_replays_the_step(route):
     """The C-ABI calls are stream-ordered and allocation-free, so one fwd+bwd
     step captures into a CUDA graph; replays give the direct results."""
     import ctypes
@@ -478,7 +504,8 @@ def test_cuda_graph_capture_replays_the_step():
     layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(3), device="cuda")
     x = torch.randn((T, N, C), device="cuda")
     dy = torch.randn((T, N, C), device="cuda")
-    desc = L.make_desc(x.shape, k, d, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS)
+    extra = L.PSN_STREAM if route == "stream" else 0
+    desc = L.make_desc(x.shape, k, d, torch.float32, flags=L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS | extra)
     ws = L.workspace(desc, x.device)
     out, dx = torch.empty_like(x), torch.empty_like(x)
     fold = torch.empty((C, L.fold_stride(k)), dtype=torch.float64, device="cuda")

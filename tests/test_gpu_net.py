@@ -141,13 +141,19 @@ def test_readout_kernels_against_reference_recurrence():
         assert_close_scaled(ro.W.grad.cpu().numpy(), np.einsum("tno,tnc->oc", dcur, xd), 1e-12, f"dW {dt}")
 
 
-def test_f32_network_trains_on_the_streamed_kernels():
-    """The production setting: f32 activations through the streamed PSN
-    kernels; the step runs, its loss tracks the f64 reference's, and training
-    reduces the loss on a fixed batch."""
+@pytest.mark.parametrize("method", ["stream", "auto"])
+def test_f32_network_trains(method):
+    """The production setting: f32 activations through the PSN kernels (the
+    streamed ones, and the planner's choice: the three generic launches at
+    this small shape); the step runs, its loss tracks the f64 reference's, and
+    training reduces the loss on a fixed batch."""
+    import paper_2501_14490_b200 as P
     from paper_2501_14490_b200.net import Adam
     z = _z()
     net = _net()
+    for layer in net.layers:
+        if isinstance(layer, P.SpikingLayer):
+            layer.configure(P.layer.LayerMethod(method))
     x = torch.tensor(z["s0_x"], device="cuda", dtype=torch.float32)
     y = torch.tensor(z["s0_y"], device="cuda")
     loss0, _ = net.train_step_grads(x, y)
@@ -208,7 +214,7 @@ def test_explicit_layer_backward_matches_autograd():
         assert torch.equal(pa.grad, pb.grad)
     b.backward(dy)  # accumulates like the reference's +=
     assert torch.equal(b.W.grad, 2 * a.W.grad)
-    assert [m.name for m in b.method_candidates()] == ["stream", "generic"]
+    assert [m.name for m in b.method_candidates()] == ["auto", "stream", "generic"]
     with pytest.raises(ValueError):
         b.configure(P.layer.LayerMethod("matmul"))
 
