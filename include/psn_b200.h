@@ -23,6 +23,7 @@
  *   psn_quantize_pow2           quant.quantize_pow2                   quant.py:111-139
  *   psn_readout_reduce  ReadoutLayer.forward (leaky accumulator)      network.py:399-419
  *   psn_readout_expand  ReadoutLayer.backward (dcur -> dx)            network.py:421-436
+ *   psn_adam_step       Adam.step over all parameter tensors           train.py:147-172
  *
  * Tensor layout: time-first, contiguous [T, N, C, Q] where Q is the product of
  * the spatial axes (1 for rank-3 [T, N, C]); reference tensor.py:71-81.
@@ -185,6 +186,25 @@ PSN_API int psn_readout_reduce(int64_t T, int64_t N, int64_t C, int32_t dtype, d
                                const void *x, double *xbar, psn_stream_t stream);
 PSN_API int psn_readout_expand(int64_t T, int64_t N, int64_t C, int32_t dtype, double tau,
                                const double *g, void *dx, psn_stream_t stream);
+
+/* ---- Adam (train.py:147-172) -------------------------------------------- */
+/* One chunk = n contiguous float64 elements of a parameter, its gradient and
+ * its two moment buffers.  The table lives in device memory (one block per
+ * chunk).  The update is the reference's element-wise sequence, bitwise:
+ *   m = m b1 + (1-b1) g;  v = v b2 + ((1-b2) g) g;
+ *   p -= (lr (m / c1)) / (sqrt(v / c2) + eps)
+ * with c1, c2 = 1 - beta^t from the host, or, when t_dev is non-null, from
+ * the device step count *t_dev (for a step captured in a CUDA graph).      */
+typedef struct {
+  double *param;
+  const double *grad;
+  double *m;
+  double *v;
+  int64_t n;
+} psn_adam_chunk_t;
+PSN_API int psn_adam_step(const psn_adam_chunk_t *chunks, int64_t n_chunks, double lr, double beta1,
+                          double beta2, double eps, double c1, double c2, const double *t_dev,
+                          psn_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libpsn_b200.so")
 SOURCES = ["psn_layer.cu", "psn_engines.cu", "psn_stream.cu", "psn_stream_f32_fwd.cu", "psn_stream_f32_bwd.cu",
-           "psn_stream_bf16_fwd.cu", "psn_stream_bf16_bwd.cu", "psn_readout.cu"]
+           "psn_stream_bf16_fwd.cu", "psn_stream_bf16_bwd.cu", "psn_readout.cu", "psn_optim.cu"]
 HEADERS = ["psn_common.cuh", "psn_stream.cuh", "psn_stream_inst.cuh", "psn_stream_dispatch.h"]
 
 NVCC_FLAGS = [

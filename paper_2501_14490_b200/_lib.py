@@ -40,7 +40,7 @@ EXPORTED = (
     "psn_workspace_bytes", "psn_forward_train", "psn_backward", "psn_forward_eval",
     "psn_conv_forward", "psn_conv_forward_shift", "psn_conv_forward_shift_int",
     "psn_conv_backward_input", "psn_conv_backward_weight", "psn_conv_backward_bias",
-    "psn_quantize_pow2", "psn_plan_info", "psn_readout_reduce", "psn_readout_expand",
+    "psn_quantize_pow2", "psn_plan_info", "psn_readout_reduce", "psn_readout_expand", "psn_adam_step",
 )
 
 
@@ -76,6 +76,8 @@ _SIGS = {
                                           ctypes.c_double, _P, _P, _P]),
     "psn_readout_expand": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                           ctypes.c_double, _P, _P, _P]),
+    "psn_adam_step": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _P]),
 }
 
 _lib = None

@@ -34,9 +34,42 @@ from .layer import Mode, ShiftLayer, SpikingLayer
 from .neuron import NeuronConfig, QuantGradMode, SurrogateConfig, WeightSharing, sawtooth_schedule
 
 
+class _LinearF32(torch.autograd.Function):
+    """The synapse on an f32 carrier with a backward shaped for its long
+    reduction (T*N rows, a few hundred columns): the weight gradient as a
+    split-K batched GEMM (S slices of the rows, partial products summed in a
+    fixed order), the bias gradient as a ones-vector GEMV.  cuBLAS's single
+    GEMM for dW = dy^T x puts one 128x128 output tile on a handful of SMs
+    (SHD shape: 107 -> 36 us for 128x128, 223 -> 120 us for 128x700;
+    scripts/mb_linear_bwd.py)."""
+
+    @staticmethod
+    def forward(ctx, x, W, b):
+        W32 = W.to(x.dtype)
+        ctx.save_for_backward(x, W32)
+        return F.linear(x, W32, b.to(x.dtype))
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, W32 = ctx.saved_tensors
+        out_f, in_f = W32.shape
+        R = x.numel() // in_f
+        g2 = gy.reshape(R, out_f)
+        x2 = x.reshape(R, in_f)
+        dx = (g2 @ W32).reshape(x.shape) if ctx.needs_input_grad[0] else None
+        S = next((s for s in (32, 16, 8, 4, 2) if R % s == 0 and R // s >= 256), 1)
+        if S > 1:
+            dW = torch.bmm(g2.view(S, R // S, out_f).transpose(1, 2), x2.view(S, R // S, in_f)).sum(0)
+        else:
+            dW = g2.t() @ x2
+        db = (torch.ones((1, R), dtype=g2.dtype, device=g2.device) @ g2).view(out_f)
+        return dx, dW.to(torch.float64), db.to(torch.float64)
+
+
 class LinearLayer(nn.Module):
     """One weight matrix shared across all time steps (network.py:80-140);
-    rank-3 time-first inputs [T, N, in] -> [T, N, out]."""
+    rank-3 time-first inputs [T, N, in] -> [T, N, out].  f32 CUDA carriers
+    take the split-K weight-gradient backward (_LinearF32)."""
 
     def __init__(self, in_features: int, out_features: int, rng: np.random.Generator | None = None,
                  *, device=None):
@@ -55,6 +88,8 @@ class LinearLayer(nn.Module):
             raise ValueError("linear layers take rank-3 tensors")
         if mode is Mode.EVAL:  # deployment path in f32 (network.py:113-116)
             return F.linear(x.to(torch.float32), self.W.to(torch.float32), self.b.to(torch.float32))
+        if x.is_cuda and x.dtype == torch.float32:
+            return _LinearF32.apply(x.contiguous(), self.W, self.b)
         return F.linear(x, self.W.to(x.dtype), self.b.to(x.dtype))
 
 
@@ -208,7 +243,12 @@ class SGD:
 class Adam:
     """The reference's Adam (train.py:147-172), the same element-wise
     operations in the same order, so the update is bit-identical for the same
-    gradients (IEEE f64 element-wise arithmetic)."""
+    gradients (IEEE f64 element-wise arithmetic).  CUDA float64 parameters
+    are updated by one launch for all tensors (psn_adam_step over a device
+    table of 4096-element chunks); CPU parameters by the element-wise torch
+    formulation."""
+
+    CHUNK = 4096
 
     def __init__(self, params, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
         self.params = list(params)
@@ -216,6 +256,29 @@ class Adam:
         self.t = 0
         self._state = {}
         self._t_dev = None  # capturable mode: the step count lives on the device
+        self._table, self._table_key = None, None
+
+    def _fused_ok(self) -> bool:
+        return all(p.is_cuda and p.dtype == torch.float64 and p.is_contiguous() and p.grad is not None
+                   and p.grad.dtype == torch.float64 and p.grad.is_contiguous() for p in self.params)
+
+    def _chunk_table(self) -> torch.Tensor:
+        """Device table of (param, grad, m, v, n) chunks; rebuilt only when a
+        tensor moved (never inside a captured step once warmed up)."""
+        for p in self.params:
+            if id(p) not in self._state:
+                self._state[id(p)] = (torch.zeros_like(p), torch.zeros_like(p))
+        key = tuple((p.data_ptr(), p.grad.data_ptr()) for p in self.params)
+        if key != self._table_key:
+            rows = []
+            for p in self.params:
+                m, v = self._state[id(p)]
+                base = (p.data_ptr(), p.grad.data_ptr(), m.data_ptr(), v.data_ptr())
+                for off in range(0, p.numel(), self.CHUNK):
+                    rows.append([b + 8 * off for b in base] + [min(self.CHUNK, p.numel() - off)])
+            self._table = torch.tensor(rows, dtype=torch.int64, device=self.params[0].device)
+            self._table_key = key
+        return self._table
 
     def make_capturable(self) -> None:
         """Keep the step count on the device so a captured step (CUDA graph)
@@ -228,8 +291,17 @@ class Adam:
     def step(self) -> None:
         self.t += 1
         b1, b2 = self.beta1, self.beta2
-        if self._t_dev is not None:
+        dev_t = self._t_dev is not None
+        if dev_t:
             self._t_dev.add_(1.0)
+        if self.params and self._fused_ok():
+            tab = self._chunk_table()
+            p0 = self.params[0]
+            c1h, c2h = (0.0, 0.0) if dev_t else (1 - b1 ** self.t, 1 - b2 ** self.t)
+            L.run(p0, "psn_adam_step", L.ptr(tab), tab.shape[0], float(self.lr), float(b1), float(b2),
+                  float(self.eps), float(c1h), float(c2h), L.ptr(self._t_dev) if dev_t else None, L.stream_of(p0))
+            return
+        if dev_t:
             c1 = 1 - torch.pow(b1, self._t_dev)
             c2 = 1 - torch.pow(b2, self._t_dev)
         else:

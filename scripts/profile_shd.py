@@ -21,4 +21,8 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(5):
         net.train_step_grads_async(x, y); opt.step()
     torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=70))
+rows = sorted(prof.key_averages(), key=lambda e: -e.self_device_time_total)
+tot = sum(e.self_device_time_total for e in rows)
+print(f"per step: {tot / 5:.1f} us of kernels")
+for e in rows[:30]:
+    print(f"{e.self_device_time_total / 5:8.1f} us/step {e.count // 5:4d}x  {e.key[:150]}")

@@ -266,3 +266,57 @@ def test_ddp_step_two_ranks_on_product_kernels():
     for r in range(2):
         for got, w in zip(out[r], want):
             np.testing.assert_allclose(got, w, rtol=1e-12, atol=1e-14)
+
+
+def test_fused_adam_matches_the_reference_update():
+    """psn_adam_step (all tensors in one launch) against a float64 numpy
+    restatement of the reference's Adam (train.py:147-172; true division, as
+    numpy does): bit-identical with host bias corrections, and within an ulp
+    of the corrections with the device step count (device pow)."""
+    from paper_2501_14490_b200.net import Adam
+    rng = np.random.default_rng(3)
+    b1, b2, lr, eps = 0.9, 0.999, 1e-2, 1e-8
+    for capturable in (False, True):
+        ref = [rng.standard_normal(n) for n in (5000, 17, 4096, 1)]
+        ps = [torch.tensor(r, device="cuda") for r in ref]
+        ms = [np.zeros_like(r) for r in ref]
+        vs = [np.zeros_like(r) for r in ref]
+        opt = Adam(ps, lr)
+        if capturable:
+            opt.make_capturable()
+        for t in range(1, 4):
+            grads = [rng.standard_normal(r.shape) for r in ref]
+            for p, g in zip(ps, grads):
+                p.grad = torch.tensor(g, device="cuda")
+            opt.step()
+            c1, c2 = 1 - b1 ** t, 1 - b2 ** t
+            for i, g in enumerate(grads):
+                ms[i] = ms[i] * b1 + (1 - b1) * g
+                vs[i] = vs[i] * b2 + (1 - b2) * g * g
+                ref[i] = ref[i] - lr * (ms[i] / c1) / (np.sqrt(vs[i] / c2) + eps)
+            for p, r in zip(ps, ref):
+                got = p.cpu().numpy()
+                if capturable:
+                    np.testing.assert_allclose(got, r, rtol=1e-14, atol=1e-16)
+                else:
+                    assert np.array_equal(got, r), (t, float(np.abs(got - r).max()))
+
+
+def test_split_k_synapse_backward_matches_f64():
+    """The f32 synapse's split-K weight gradient and GEMV bias gradient against
+    the float64 products of the same f32 inputs (f32 accumulation over 32000
+    rows: cuBLAS's single f32 GEMM is off by up to ~3e-5 of max(|ref|, 1)
+    here too, scripts/diag_dw_f32.py)."""
+    from paper_2501_14490_b200.layer import Mode
+    from paper_2501_14490_b200.net import LinearLayer
+    lin = LinearLayer(700, 128, rng=np.random.default_rng(4), device="cuda")
+    x = (torch.rand(250, 128, 700, device="cuda") < 0.05).float().requires_grad_(True)
+    y = lin(x, Mode.TRAIN)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xd, gd = x.detach().double(), gy.double()
+    W32 = lin.W.detach().float().double()
+    assert_close_scaled(lin.W.grad.cpu().numpy(), torch.einsum("tno,tni->oi", gd, xd).cpu().numpy(), 1e-4, "dW")
+    assert_close_scaled(lin.b.grad.cpu().numpy(), gd.sum(dim=(0, 1)).cpu().numpy(), 1e-4, "db")
+    assert_close_scaled(x.grad.double().cpu().numpy(), torch.einsum("tno,oi->tni", gd, W32).cpu().numpy(), 1e-5,
+                        "dx")
