@@ -197,6 +197,26 @@ __device__ __forceinline__ double conv_taps(const double (&w)[K], const double (
   return h;
 }
 
+// the same sum as two interleaved half chains (even / odd taps) for the
+// quantities only compared under a tolerance (h1 for the statistics, h1 / h2
+// in the backward): half the dependent-DFMA latency per step, a different
+// rounding order (~1 f64 ulp) than the reference's tap order
+template <int K>
+__device__ __forceinline__ double conv_taps2(const double (&w)[K], const double (&xw)[K]) {
+  if constexpr (K < 4) {
+    return conv_taps<K>(w, xw);
+  } else {
+    double a = w[0] * xw[0], b = w[1] * xw[1];
+#pragma unroll
+    for (int i = 2; i + 1 < K; i += 2) {
+      a = fma(w[i], xw[i], a);
+      b = fma(w[i + 1], xw[i + 1], b);
+    }
+    if (K & 1) a = fma(w[K - 1], xw[K - 1], a);
+    return a + b;
+  }
+}
+
 // ------------------------------------------------------------------------------
 // forward pass 1: statistics of h1 = conv(x, W)
 // ------------------------------------------------------------------------------
@@ -229,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_stats_kernel(Ge
     double k0 = 0.0, s1 = 0.0, s2 = 0.0;  // k0: the segment's first h1, shift for the moments
     stream_any<(K > 8 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t t, int64_t) {
       push<K>(xw, wide(xv));
-      const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
+      const double h1 = Carrier<IO>::round(conv_taps2<K>(w, xw));
       if (t == s.s0) k0 = h1;
       const double dl = h1 - k0;
       s1 += dl;
@@ -502,8 +522,8 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
       const double v = wide(xv);
       push<K>(xw, v);
       xsum += v;
-      const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
-      const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps<K>(wq, xw), bf));
+      const double h1 = Carrier<IO>::round(conv_taps2<K>(w, xw));
+      const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps2<K>(wq, xw), bf));
       const double dh2 = jv ? dh2_val<IO>(sur, skind, alpha, h2, dv) : 0.0;
       const double hc = h1 - mu;
       if (dm && jv) {
@@ -693,8 +713,8 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
       Acc dh2 = (Acc)0, dh1 = (Acc)0;
       if (t < s.Sr) {
         push<K>(xw, wide(xv));
-        const double h1 = Carrier<IO>::round(conv_taps<K>(w, xw));
-        const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps<K>(wq, xw), bf));
+        const double h1 = Carrier<IO>::round(conv_taps2<K>(w, xw));
+        const double h2 = Carrier<IO>::round(__dadd_rn(conv_taps2<K>(wq, xw), bf));
         dh2 = jv ? (Acc)dh2_val<IO>(sur, skind, alpha, h2, dv) : (Acc)0;
         dh1 = (Acc)(alpha1 + beta1 * (h1 - mu));
       }
