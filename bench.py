@@ -350,6 +350,42 @@ def run_suite(P, L, dev, hbm, m=3):
         except Exception as e:  # a config that cannot run is reported, not fatal
             out[name] = {"error": str(e)[:200]}
         torch.cuda.empty_cache()
+    # SURVEY.md section 8(f) rank 1, the mul-free inference path at the metric
+    # shape: SpikingLayer EVAL (running statistics folded, pow2 taps, one
+    # spike kernel: reads x, writes spikes, 8 B/elem f32) and the quantized
+    # file's ShiftLayer (engine operator psn_conv_forward_shift, bit-exact to
+    # the reference's ldexp path, then the threshold)
+    try:
+        import numpy as np
+        T, B, C = 1024, 64, 512
+        g = torch.Generator(device=dev).manual_seed(7)
+        xe = torch.randn((T, B, C), generator=g, device=dev)
+        lay = P.SpikingLayer(P.NeuronConfig(channels=C, order=4, dilation=1, quantized=True),
+                             weight_init="uniform", rng=np.random.default_rng(1), device=dev)
+        lay.eval()
+
+        def graphed(fn):  # one CUDA graph per call, like the TRAIN workload's replay
+            fn()
+            torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                fn()
+            return gr.replay
+        sec = protocol.benchmark_candidate(graphed(lambda: lay(xe, P.Mode.EVAL)), m=m)
+        out["eval_T1024_B64_C512_k4"] = {"ms": sec * 1e3, "gsteps_ch_per_s": T * B * C / sec / 1e9,
+                                         "hbm_frac": 8 * T * B * C / sec / 1e9 / hbm,
+                                         "what": "SpikingLayer EVAL (psn_forward_eval: fold + one spike kernel), "
+                                                 "f32, CUDA-graph replay"}
+        sw, bias = lay.quantized_snapshot()
+        sl = P.ShiftLayer(sw, bias, 1)
+        sec = protocol.benchmark_candidate(graphed(lambda: sl(xe, P.Mode.EVAL)), m=m)
+        out["shift_eval_T1024_B64_C512_k4"] = {"ms": sec * 1e3, "gsteps_ch_per_s": T * B * C / sec / 1e9,
+                                               "what": "ShiftLayer (quantized model file): psn_conv_forward_shift "
+                                                       "(reference ldexp arithmetic, h written) + threshold"}
+        del xe, lay, sl
+    except Exception as e:
+        out["eval_T1024_B64_C512_k4"] = {"error": str(e)[:200]}
+    torch.cuda.empty_cache()
     for korder in (2, 4):
         T, B, IN, H = 250, 128, 700, 128
         net = build_task_net(channels=H, num_layers=3, order=korder, classes=20, seed=0, in_features=IN,
