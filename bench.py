@@ -353,8 +353,8 @@ def run_suite(P, L, dev, hbm, m=3):
     # SURVEY.md section 8(f) rank 1, the mul-free inference path at the metric
     # shape: SpikingLayer EVAL (running statistics folded, pow2 taps, one
     # spike kernel: reads x, writes spikes, 8 B/elem f32) and the quantized
-    # file's ShiftLayer (engine operator psn_conv_forward_shift, bit-exact to
-    # the reference's ldexp path, then the threshold)
+    # file's ShiftLayer (psn_shift_spike_forward: the engine's ldexp arithmetic,
+    # bit-exact to the reference, and the threshold in one pass)
     try:
         import numpy as np
         T, B, C = 1024, 64, 512
@@ -380,8 +380,9 @@ def run_suite(P, L, dev, hbm, m=3):
         sl = P.ShiftLayer(sw, bias, 1)
         sec = protocol.benchmark_candidate(graphed(lambda: sl(xe, P.Mode.EVAL)), m=m)
         out["shift_eval_T1024_B64_C512_k4"] = {"ms": sec * 1e3, "gsteps_ch_per_s": T * B * C / sec / 1e9,
-                                               "what": "ShiftLayer (quantized model file): psn_conv_forward_shift "
-                                                       "(reference ldexp arithmetic, h written) + threshold"}
+                                               "what": "ShiftLayer (quantized model file): psn_shift_spike_forward "
+                                                       "(reference ldexp arithmetic and threshold in one pass), "
+                                                       "CUDA-graph replay"}
         del xe, lay, sl
     except Exception as e:
         out["eval_T1024_B64_C512_k4"] = {"error": str(e)[:200]}

@@ -16,6 +16,7 @@
  *   psn_forward_eval    SpikingLayer._forward_eval / ShiftLayer.forward network.py:219-234, 351-359
  *   psn_conv_forward    engines.conv_forward(engine=DIRECT)            engines.py:117-138, 336-347
  *   psn_conv_forward_shift      engines.conv_forward_shift (float)    engines.py:258-294
+ *   psn_shift_spike_forward     ShiftLayer.forward (shift conv + spike) network.py:352-362
  *   psn_conv_forward_shift_int  engines.conv_forward_shift (int32)    engines.py:297-325
  *   psn_conv_backward_input     engines.conv_backward_input           engines.py:350-377
  *   psn_conv_backward_weight    engines.conv_backward_weight          engines.py:402-425
@@ -157,6 +158,11 @@ PSN_API int psn_conv_forward(const psn_desc_t *desc, const void *x, const double
 PSN_API int psn_conv_forward_shift(const psn_desc_t *desc, const void *x, const int8_t *sign,
                            const int8_t *exponent, int64_t w_rows, const double *bias,
                            void *out, psn_stream_t stream);
+/* the same membrane, thresholded in the same pass: out = (carrier(h) >= 0) as
+ * 0 / 1 in the carrier dtype (the deserialised quantized model's layer).      */
+PSN_API int psn_shift_spike_forward(const psn_desc_t *desc, const void *x, const int8_t *sign,
+                            const int8_t *exponent, int64_t w_rows, const double *bias,
+                            void *out, psn_stream_t stream);
 /* int32 carrier: arithmetic shifts, int64 accumulation, bias truncated to
  * int64, clip to int32; *saturations (device u64) incremented per clip.      */
 PSN_API int psn_conv_forward_shift_int(const psn_desc_t *desc, const int32_t *x, const int8_t *sign,

@@ -41,6 +41,7 @@ EXPORTED = (
     "psn_conv_forward", "psn_conv_forward_shift", "psn_conv_forward_shift_int",
     "psn_conv_backward_input", "psn_conv_backward_weight", "psn_conv_backward_bias",
     "psn_quantize_pow2", "psn_plan_info", "psn_readout_reduce", "psn_readout_expand", "psn_adam_step",
+    "psn_shift_spike_forward",
 )
 
 
@@ -66,6 +67,7 @@ _SIGS = {
     "psn_forward_eval": (ctypes.c_int, [_D, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psn_conv_forward": (ctypes.c_int, [_D, _P, _P, ctypes.c_int64, _P, _P, _P]),
     "psn_conv_forward_shift": (ctypes.c_int, [_D, _P, _P, _P, ctypes.c_int64, _P, _P, _P]),
+    "psn_shift_spike_forward": (ctypes.c_int, [_D, _P, _P, _P, ctypes.c_int64, _P, _P, _P]),
     "psn_conv_forward_shift_int": (ctypes.c_int, [_D, _P, _P, _P, ctypes.c_int64, _P, _P, _P, _P]),
     "psn_conv_backward_input": (ctypes.c_int, [_D, _P, _P, ctypes.c_int64, _P, _P]),
     "psn_conv_backward_weight": (ctypes.c_int, [_D, _P, _P, ctypes.c_int, _P, _P, _P]),

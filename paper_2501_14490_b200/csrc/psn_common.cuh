@@ -376,6 +376,16 @@ int validate(const psn_desc_t* d, bool allow_i32);
 int check_ptr(const void* p, size_t align, const char* what);
 size_t dtype_size(int dt);
 size_t workspace_part3_offset(const psn_desc_t* desc);
+
+// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
+template <typename Kern>
+int smem_optin(Kern* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return PSN_OK;
+  if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (generic kernel smem) failed");
+  return PSN_OK;
+}
 size_t workspace_dwtmp_offset(const psn_desc_t* desc);
 
 }  // namespace psn

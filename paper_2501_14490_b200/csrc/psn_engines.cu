@@ -13,9 +13,12 @@
 
 namespace psn {
 
-// forward conv with float weights (SHIFT=false) or sign/exponent weights
-template <int K, typename IO, bool SHIFT>
-__global__ void __launch_bounds__(kThreads) eng_fwd_kernel(Geom g, const IO* __restrict__ x,
+// forward conv with float weights (SHIFT=false) or sign/exponent weights;
+// SPIKE: the ShiftLayer's Heaviside fused on the carrier-rounded membrane
+// (network.py:352-362: spikes = (f32(h) >= 0), no h written).  Streams x through
+// the per-warp shared-memory ring (psn_common.cuh stream_any).
+template <int K, typename IO, bool SHIFT, bool SPIKE = false>
+__global__ void __launch_bounds__(kThreads, 2) eng_fwd_kernel(Geom g, const IO* __restrict__ x,
                                                            const double* __restrict__ w,
                                                            const int8_t* __restrict__ sgn,
                                                            const int8_t* __restrict__ ex,
@@ -39,6 +42,9 @@ __global__ void __launch_bounds__(kThreads) eng_fwd_kernel(Geom g, const IO* __r
   const bool hb = bias != nullptr;
   const double b = (jv && hb) ? bias[c] : 0.0;
   const int64_t step = (int64_t)g.d * g.row;
+  extern __shared__ __align__(16) unsigned char psn_dsm[];
+  IO* ring = reinterpret_cast<IO*>(psn_dsm) + warp * kRingSteps * 32;
+  const ColTile ct = col_tile<IO>(g, x, x);
   for (int64_t seg = (int64_t)blockIdx.y * kWarps + warp; seg < g.nseg; seg += (int64_t)gridDim.y * kWarps) {
     Seg s;
     if (!decode_seg(g, seg, s)) continue;
@@ -51,18 +57,21 @@ __global__ void __launch_bounds__(kThreads) eng_fwd_kernel(Geom g, const IO* __r
     }
     const IO* p = x + off + s.s0 * step;
     IO* o = out + off + s.s0 * step;
-    for (int64_t t = s.s0; t < s.s1; ++t) {
+    stream_any<(K > 8 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t, int64_t eo) {
 #pragma unroll
       for (int i = 0; i < K - 1; ++i) xw[i] = xw[i + 1];
-      xw[K - 1] = jv ? load_wide(p) : 0.0;
+      xw[K - 1] = wide(xv);
       double h = 0.0;
 #pragma unroll
       for (int i = 0; i < K; ++i) h = __dadd_rn(h, __dmul_rn(wv[i], xw[i]));
       if (hb) h = __dadd_rn(h, b);
-      if (jv) Carrier<IO>::store(o, h);
-      p += step;
-      o += step;
-    }
+      if (jv) {
+        if (SPIKE)
+          Carrier<IO>::storef(o + eo, Carrier<IO>::round(h) >= 0.0 ? 1.0f : 0.0f);
+        else
+          Carrier<IO>::store(o + eo, h);
+      }
+    });
   }
 }
 
@@ -321,10 +330,12 @@ int psn_conv_forward(const psn_desc_t* desc, const void* x, const double* w, int
   const Geom g = plan(desc);
   cudaStream_t st = (cudaStream_t)stream;
   if (desc->dtype == PSN_F32) {
-    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, float, false><<<grid_map(g), kThreads, 0, st>>>(
+    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, float, false><<<grid_map(g), kThreads, ring_bytes<float>(1), st>>>(
                               g, (const float*)x, w, nullptr, nullptr, w_rows, bias, (float*)out)));
   } else {
-    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, double, false><<<grid_map(g), kThreads, 0, st>>>(
+    PSN_K_SWITCH(desc->k, (rc = smem_optin(eng_fwd_kernel<K, double, false>, ring_bytes<double>(1))));
+    if (rc) return rc;
+    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, double, false><<<grid_map(g), kThreads, ring_bytes<double>(1), st>>>(
                               g, (const double*)x, w, nullptr, nullptr, w_rows, bias, (double*)out)));
   }
   return cuda_check("psn_conv_forward");
@@ -341,13 +352,39 @@ int psn_conv_forward_shift(const psn_desc_t* desc, const void* x, const int8_t* 
   const Geom g = plan(desc);
   cudaStream_t st = (cudaStream_t)stream;
   if (desc->dtype == PSN_F32) {
-    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, float, true><<<grid_map(g), kThreads, 0, st>>>(
+    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, float, true><<<grid_map(g), kThreads, ring_bytes<float>(1), st>>>(
                               g, (const float*)x, nullptr, sign, exponent, w_rows, bias, (float*)out)));
   } else {
-    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, double, true><<<grid_map(g), kThreads, 0, st>>>(
+    PSN_K_SWITCH(desc->k, (rc = smem_optin(eng_fwd_kernel<K, double, true>, ring_bytes<double>(1))));
+    if (rc) return rc;
+    PSN_K_SWITCH(desc->k, (eng_fwd_kernel<K, double, true><<<grid_map(g), kThreads, ring_bytes<double>(1), st>>>(
                               g, (const double*)x, nullptr, sign, exponent, w_rows, bias, (double*)out)));
   }
   return cuda_check("psn_conv_forward_shift");
+}
+
+int psn_shift_spike_forward(const psn_desc_t* desc, const void* x, const int8_t* sign, const int8_t* exponent,
+                            int64_t w_rows, const double* bias, void* out, psn_stream_t stream) {
+  int rc;
+  if ((rc = validate(desc, false)) || (rc = check_float_carrier(desc)) || (rc = check_rows(desc, w_rows))) return rc;
+  const size_t es = dtype_size(desc->dtype);
+  if ((rc = check_ptr(x, es, "x")) || (rc = check_ptr(out, es, "out")) || (rc = check_ptr(sign, 1, "sign")) ||
+      (rc = check_ptr(exponent, 1, "exponent")))
+    return rc;
+  const Geom g = plan(desc);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (desc->dtype == PSN_F32) {
+    PSN_K_SWITCH(desc->k,
+                 (eng_fwd_kernel<K, float, true, true><<<grid_map(g), kThreads, ring_bytes<float>(1), st>>>(
+                     g, (const float*)x, nullptr, sign, exponent, w_rows, bias, (float*)out)));
+  } else {
+    PSN_K_SWITCH(desc->k, (rc = smem_optin(eng_fwd_kernel<K, double, true, true>, ring_bytes<double>(1))));
+    if (rc) return rc;
+    PSN_K_SWITCH(desc->k,
+                 (eng_fwd_kernel<K, double, true, true><<<grid_map(g), kThreads, ring_bytes<double>(1), st>>>(
+                     g, (const double*)x, nullptr, sign, exponent, w_rows, bias, (double*)out)));
+  }
+  return cuda_check("psn_shift_spike_forward");
 }
 
 int psn_conv_forward_shift_int(const psn_desc_t* desc, const int32_t* x, const int8_t* sign,

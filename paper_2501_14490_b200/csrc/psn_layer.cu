@@ -789,15 +789,6 @@ __global__ void __launch_bounds__(kThreads, 2) bwd_dx_mat_kernel(Geom g, const f
 // ------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------
-// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
-template <typename Kern>
-int smem_optin(Kern* kern, size_t bytes) {
-  if (bytes <= 48 * 1024) return PSN_OK;
-  if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
-      cudaSuccess)
-    return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (generic kernel smem) failed");
-  return PSN_OK;
-}
 inline dim3 grid_red(const Geom& g) { return dim3((unsigned)g.ctiles, (unsigned)g.rows); }
 inline dim3 grid_map(const Geom& g) {
   int64_t y = (g.nseg + kWarps - 1) / kWarps;

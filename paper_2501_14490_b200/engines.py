@@ -132,6 +132,28 @@ def conv_forward_shift(x: torch.Tensor, w: ShiftWeights, bias=None, d: int = 1) 
     return conv_forward(x, w, bias, d)
 
 
+def shift_spike_forward(x: torch.Tensor, w: ShiftWeights, bias=None, d: int = 1) -> torch.Tensor:
+    """The quantized model layer's forward in one pass (src/network.py:352-362):
+    spikes = (carrier(conv_forward_shift(x, w, bias, d)) >= 0), 0 / 1 in the
+    carrier dtype (f32 or f64), bit-identical to the two-step composition."""
+    if not isinstance(w, ShiftWeights):
+        raise TypeError("shift engine requires ShiftWeights")
+    if d < 1:
+        raise ValueError(f"dilation must be >= 1, got {d}")
+    x = _carrier(x)
+    C = x.shape[2]
+    sign = w.sign.to(x.device).contiguous()
+    expo = w.exponent.to(x.device).contiguous()
+    if sign.dim() != 2 or sign.shape[0] not in (1, C):
+        raise ValueError(f"weight rows {sign.shape[0]} do not match {C} channels")
+    b = _bias(bias, C, x.device)
+    desc = L.make_desc(x.shape, sign.shape[1], d, x.dtype)
+    out = torch.empty_like(x)
+    L.run(x, "psn_shift_spike_forward", ctypes.byref(desc), L.ptr(x), L.ptr(sign), L.ptr(expo), sign.shape[0],
+          L.ptr(b), L.ptr(out), L.stream_of(x))
+    return out
+
+
 def conv_forward_shift_int(x: torch.Tensor, w: ShiftWeights, bias=None, d: int = 1):
     """int32 fixed-point shift engine; returns (out int32, saturation count)
     (src/engines.py:297-325)."""

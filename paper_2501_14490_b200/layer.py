@@ -31,7 +31,7 @@ import torch
 from torch import nn
 
 from . import _lib as L
-from .engines import ShiftWeights, conv_forward_shift
+from .engines import ShiftWeights, shift_spike_forward
 from .neuron import (BN_EPS_DEFAULT, BN_MOMENTUM_DEFAULT, NeuronConfig, QuantGradMode,
                      SurrogateConfig, SurrogateKind, WeightSharing, init_weights)
 
@@ -277,8 +277,7 @@ class ShiftLayer(nn.Module):
             raise ValueError("quantized fused layers are inference-only")
         L.require_cuda(x)
         x32 = x.to(torch.float32).contiguous()
-        h = conv_forward_shift(x32, self.sw, bias=self.bias.to(x32.device, torch.float64), d=self.dilation)
-        return (h >= 0).to(torch.float32)
+        return shift_spike_forward(x32, self.sw, bias=self.bias.to(x32.device, torch.float64), d=self.dilation)
 
     def backward(self, dy):
         raise ValueError("quantized fused layers are inference-only")

@@ -127,3 +127,25 @@ def test_spatial_axes(shape):
     dh = rng.standard_normal(shape)
     assert_close_scaled(P.conv_backward_weight(_t(x), _t(dh), 2, 2).cpu().numpy(),
                         O.conv_backward_weight(x, dh, 2, 2), 1e-12, "spatial bwd_w")
+
+
+@pytest.mark.parametrize("shape,k,d,rows,dt", [((300, 7, 45), 4, 2, 45, torch.float32),
+                                               ((64, 16, 128), 16, 3, 1, torch.float32),
+                                               ((50, 4, 6, 3, 3), 3, 1, 6, torch.float64)])
+def test_shift_spike_forward_is_the_two_step_composition(shape, k, d, rows, dt):
+    """psn_shift_spike_forward (the quantized model layer in one pass) equals
+    the reference's two steps, conv_forward_shift then (h >= 0), bit for bit,
+    including exact-zero membranes (integer inputs)."""
+    from paper_2501_14490_b200.engines import ShiftWeights, conv_forward_shift, shift_spike_forward
+    g = torch.Generator().manual_seed(sum(shape) + k)
+    sign = torch.randint(-1, 2, (rows, k), generator=g, dtype=torch.int8)
+    expo = torch.randint(-3, 3, (rows, k), generator=g, dtype=torch.int8)
+    sw = ShiftWeights(sign, expo)
+    C = shape[2]
+    bias = torch.randint(-2, 3, (C,), generator=g).double() * 0.5
+    x = torch.randint(-3, 4, shape, generator=g).to(dt).cuda()
+    two = (conv_forward_shift(x, sw, bias=bias, d=d) >= 0).to(dt)
+    one = shift_spike_forward(x, sw, bias=bias, d=d)
+    assert one.dtype == dt and torch.equal(one, two)
+    xr = torch.randn(shape, generator=g).to(dt).cuda()
+    assert torch.equal(shift_spike_forward(xr, sw, bias=bias, d=d), (conv_forward_shift(xr, sw, bias=bias, d=d) >= 0).to(dt))
