@@ -540,3 +540,14 @@ def test_cuda_graph_capture_replays_the_step(route):
         assert torch.equal(got, want)
     assert torch.equal(layer.running_mean, ref_stats[0])
     assert torch.equal(layer.running_var, ref_stats[1])
+
+
+@pytest.mark.parametrize("method", ["stream", "generic"])
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("k", list(range(1, 17)))
+def test_order_dilation_sweep(k, d, method):
+    """Every order 1..16 at every sawtooth dilation, on both kernel families
+    (the streamed method falls back to the generic kernels where the shape
+    does not qualify: k > 8), every channel against the oracle; T off the
+    time-tile grid, B off the batch-tile grid."""
+    _oracle_subset_check(203, 11, 64, k, d, channels=list(range(64)), seed=1000 + 10 * k + d, method=method)
