@@ -551,3 +551,12 @@ def test_order_dilation_sweep(k, d, method):
     does not qualify: k > 8), every channel against the oracle; T off the
     time-tile grid, B off the batch-tile grid."""
     _oracle_subset_check(203, 11, 64, k, d, channels=list(range(64)), seed=1000 + 10 * k + d, method=method)
+
+
+@pytest.mark.parametrize("method", ["stream", "generic"])
+@pytest.mark.parametrize("k,d", [(2, 1), (4, 3), (8, 2), (16, 1), (16, 3)])
+def test_bf16_order_sweep(k, d, method):
+    """bf16 I/O across orders and dilations on both kernel families (bf16 dx
+    bound: half a bf16 ulp plus the f32 bound)."""
+    _oracle_subset_check(150, 9, 96, k, d, channels=list(range(96)), dtype=torch.bfloat16, seed=2000 + 10 * k + d,
+                         method=method)
