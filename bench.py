@@ -57,52 +57,70 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+period = float(sys.argv[2])
+print("ready", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+          pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    time.sleep(period)
+"""
+
+
 class ClockSampler:
-    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+    """NVML SM-clock / throttle-reason sampler running during the timed region,
+    in its own process (a sampling thread would wait for the GIL while the
+    benchmark thread launches and synchronises; one NVML clock query takes
+    ~0.5 ms on the box)."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period_s: float = 0.002):
+    def __init__(self, index: int, period_s: float = 0.0002):
         self.samples, self.reasons = [], set()
-        self.period = period_s
-        self._stop = threading.Event()
+        self.index, self.period = index, period_s
+        self.max_mhz = None
+        self.proc = None
         self.ok = False
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception:
-            self.max_mhz = None
-
-    def _run(self):
-        nv = self.nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
 
     def __enter__(self):
-        if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index), str(self.period)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            if first and first[0] == "ready":
+                self.max_mhz = int(first[1])
+                self.ok = True
+        except Exception:
+            self.ok = False
         return self
 
     def __exit__(self, *a):
-        if self.ok:
-            self._stop.set()
-            self.t.join()
+        if self.proc is None:
+            return
+        self.proc.terminate()  # the sampler process this object started (exact PID)
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            parts = line.split()
+            if len(parts) != 2:
+                continue
+            try:
+                mhz, r = int(parts[0]), int(parts[1])
+            except ValueError:
+                continue
+            self.samples.append(mhz)
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    self.reasons.add(name)
 
     def summary(self):
         if not self.ok or not self.samples:
