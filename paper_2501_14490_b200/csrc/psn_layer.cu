@@ -277,6 +277,22 @@ __global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_stats_kernel(Ge
   }
 }
 
+// (partial row, spatial column) of flat index idx = r Q + q, advanced by 32 per
+// lane step without a division in the loop (the folds walk rows * Q partials)
+struct RowCol {
+  int64_t r;
+  int q, Q, dr, dq;
+  __device__ RowCol(int lane, int Q_) : r(lane / Q_), q(lane % Q_), Q(Q_), dr(32 / Q_), dq(32 % Q_) {}
+  __device__ void next() {
+    r += dr;
+    q += dq;
+    if (q >= Q) {
+      q -= Q;
+      ++r;
+    }
+  }
+};
+
 // ------------------------------------------------------------------------------
 // forward fold: one warp per channel (deterministic merge order)
 // ------------------------------------------------------------------------------
@@ -294,9 +310,9 @@ __global__ void __launch_bounds__(kThreads) fwd_fold_kernel(Geom g, const double
   const int K = g.k;
   Moments acc{0.0, 0.0, 0.0};
   const int64_t total = g.rows * g.Q;
-  for (int64_t idx = lane; idx < total; idx += 32) {
-    const int64_t r = idx / g.Q, q = idx % g.Q;
-    const double* p = part + r * 3 * g.J + c * g.Q + q;
+  RowCol rq(lane, (int)g.Q);
+  for (int64_t idx = lane; idx < total; idx += 32, rq.next()) {
+    const double* p = part + rq.r * 3 * g.J + c * g.Q + rq.q;
     acc = merge(acc, Moments{p[0], p[g.J], p[2 * g.J]});
   }
 #pragma unroll
@@ -599,10 +615,9 @@ __global__ void __launch_bounds__(kThreads) bwd_fold_kernel(Geom g, const double
   const int64_t total = g.rows * g.Q;
   for (int v = warp; v < NV; v += kWarps) {
     double acc = 0.0;
-    for (int64_t idx = lane; idx < total; idx += 32) {
-      const int64_t r = idx / g.Q, q = idx % g.Q;
-      acc += part[(r * NV + v) * g.J + c * g.Q + q];
-    }
+    RowCol rq(lane, (int)g.Q);
+    for (int64_t idx = lane; idx < total; idx += 32, rq.next())
+      acc += part[(rq.r * NV + v) * g.J + c * g.Q + rq.q];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       const double o = __shfl_xor_sync(0xffffffffu, acc, off);
