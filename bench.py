@@ -64,17 +64,19 @@ h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 period = float(sys.argv[2])
 print("ready", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
 while True:
-    print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-          pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(time.time(), mhz, r, flush=True)
     time.sleep(period)
 """
 
 
 class ClockSampler:
-    """NVML SM-clock / throttle-reason sampler running during the timed region,
-    in its own process (a sampling thread would wait for the GIL while the
-    benchmark thread launches and synchronises; one NVML clock query takes
-    ~0.5 ms on the box)."""
+    """NVML SM-clock / throttle-reason sampler around the timed region, in its
+    own process (a sampling thread would wait for the GIL while the benchmark
+    thread launches and synchronises; one NVML clock query takes ~0.1-0.5 ms).
+    Samples carry wall-clock stamps; the summary uses those taken inside the
+    timed region, and the sampler runs until one sample lands after it."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -82,11 +84,16 @@ class ClockSampler:
                0x100: "display_clock_setting"}
 
     def __init__(self, index: int, period_s: float = 0.0002):
-        self.samples, self.reasons = [], set()
         self.index, self.period = index, period_s
         self.max_mhz = None
         self.proc = None
         self.ok = False
+        self.lines = []
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            self.lines.append(line)
 
     def __enter__(self):
         try:
@@ -96,38 +103,53 @@ class ClockSampler:
             if first and first[0] == "ready":
                 self.max_mhz = int(first[1])
                 self.ok = True
+                self.rt = threading.Thread(target=self._reader, daemon=True)
+                self.rt.start()
         except Exception:
             self.ok = False
+        self.t0 = time.time()
         return self
 
+    def _parsed(self):
+        out = []
+        for line in list(self.lines):
+            parts = line.split()
+            if len(parts) == 3:
+                try:
+                    out.append((float(parts[0]), int(parts[1]), int(parts[2])))
+                except ValueError:
+                    pass
+        return out
+
     def __exit__(self, *a):
+        self.t1 = time.time()
         if self.proc is None:
             return
+        if self.ok:  # keep sampling until one sample is stamped after the region (<= 0.5 s)
+            deadline = time.time() + 0.5
+            while time.time() < deadline and not any(t >= self.t1 for t, _, _ in self._parsed()):
+                time.sleep(0.001)
         self.proc.terminate()  # the sampler process this object started (exact PID)
         try:
-            out, _ = self.proc.communicate(timeout=10)
+            self.proc.wait(timeout=10)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-            out, _ = self.proc.communicate()
-        for line in out.splitlines():
-            parts = line.split()
-            if len(parts) != 2:
-                continue
-            try:
-                mhz, r = int(parts[0]), int(parts[1])
-            except ValueError:
-                continue
-            self.samples.append(mhz)
-            for bit, name in self.REASONS.items():
-                if r & bit and bit != 0x1:
-                    self.reasons.add(name)
+            self.proc.wait()
+        if self.ok:
+            self.rt.join(timeout=5)
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": len(self.samples)}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        s = self._parsed() if self.ok else []
+        inside = [x for x in s if self.t0 <= x[0] <= self.t1]
+        use = inside or [min(s, key=lambda x: abs(x[0] - self.t1))] if s else []
+        reasons = set()
+        for _, _, r in use:
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(m for _, m, _ in use) if use else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(inside),
+                "samples_total": len(s), "region_ms": round((self.t1 - self.t0) * 1e3, 2)}
 
 
 # --------------------------------------------------------------------------
