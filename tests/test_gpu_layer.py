@@ -560,3 +560,14 @@ def test_bf16_order_sweep(k, d, method):
     bound: half a bf16 ulp plus the f32 bound)."""
     _oracle_subset_check(150, 9, 96, k, d, channels=list(range(96)), dtype=torch.bfloat16, seed=2000 + 10 * k + d,
                          method=method)
+
+
+@pytest.mark.parametrize("method", ["stream", "generic"])
+@pytest.mark.parametrize("shape,k,d", [((5, 1, 1), 16, 3), ((1, 3, 5), 1, 1), ((2, 2, 33), 4, 2),
+                                        ((40, 1, 3, 7), 5, 2), ((17, 2, 2, 5, 3), 3, 3), ((64, 33, 37), 2, 1)])
+def test_odd_shapes(shape, k, d, method):
+    """Degenerate and ragged extents on both kernel families: T = 1, T < halo,
+    N = 1, C = 1, J not a multiple of the 16-byte piece, odd spatial axes."""
+    T, N, C = shape[:3]
+    _oracle_subset_check(T, N, C, k, d, channels=list(range(C)), seed=sum(shape) + 3 * k + d, spatial=shape[3:],
+                         method=method)
