@@ -571,3 +571,55 @@ def test_odd_shapes(shape, k, d, method):
     T, N, C = shape[:3]
     _oracle_subset_check(T, N, C, k, d, channels=list(range(C)), seed=sum(shape) + 3 * k + d, spatial=shape[3:],
                          method=method)
+
+
+@pytest.mark.parametrize("method", ["auto", "generic"])
+def test_float64_carrier_medium_shape(method):
+    """float64 carrier (generic kernels: 8-byte ring elements, 16-byte pieces of
+    two columns) at a medium shape, every channel against the oracle run on
+    the same f64 inputs; f64 tolerance."""
+    P = _P()
+    T, N, C, k, d = 200, 9, 64, 4, 2
+    rng = np.random.default_rng(77)
+    x_np = rng.standard_normal((T, N, C))
+    dy_np = rng.standard_normal((T, N, C))
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(78), device="cuda")
+    layer.configure(P.layer.LayerMethod(method))
+    x = torch.tensor(x_np, device="cuda", requires_grad=True)
+    out = layer(x, P.Mode.TRAIN)
+    out.backward(torch.tensor(dy_np, device="cuda"))
+    p = O.init_layer(C, k, d, weight_init="uniform", rng=np.random.default_rng(78))
+    p.W = layer.W.detach().cpu().numpy()
+    ref_out, cache, dx, dW, dg, db = O.train_step(p, x_np, dy_np)
+    spikes_match_except_ties(out.detach().cpu().numpy(), ref_out, x_np, cache.w_q, cache.b_f, d)
+    assert_close_scaled(x.grad.cpu().numpy(), dx, 1e-9, "dx")
+    assert_close_scaled(layer.W.grad.cpu().numpy(), dW, 1e-9, "dW")
+    assert_close_scaled(layer.gamma.grad.cpu().numpy(), dg, 1e-9, "dgamma")
+    assert_close_scaled(layer.beta.grad.cpu().numpy(), db, 1e-9, "dbeta")
+
+
+@pytest.mark.parametrize("method", ["auto", "generic"])
+def test_smooth_mode_medium_shape(method):
+    """SMOOTH mode (spike primitive output, statistics frozen; generic kernels)
+    at a medium shape against the oracle."""
+    P = _P()
+    T, N, C, k, d = 150, 8, 96, 3, 3
+    rng = np.random.default_rng(88)
+    x_np = rng.standard_normal((T, N, C)).astype(np.float32)
+    dy_np = rng.standard_normal((T, N, C)).astype(np.float32)
+    cfg = P.NeuronConfig(channels=C, order=k, dilation=d, quantized=True)
+    layer = P.SpikingLayer(cfg, weight_init="uniform", rng=np.random.default_rng(89), device="cuda")
+    layer.configure(P.layer.LayerMethod(method))
+    x = torch.tensor(x_np, device="cuda", requires_grad=True)
+    out = layer(x, P.Mode.SMOOTH)
+    out.backward(torch.tensor(dy_np, device="cuda"))
+    p = O.init_layer(C, k, d, weight_init="uniform", rng=np.random.default_rng(89))
+    p.W = layer.W.detach().cpu().numpy()
+    ref_out, cache = O.forward_train(p, x_np, smooth=True)
+    dx, dW, dg, db = O.backward(p, cache, dy_np)
+    assert_close_scaled(out.detach().cpu().numpy(), ref_out, 1e-6, "smooth output")
+    assert_close_scaled(x.grad.cpu().numpy(), dx, 1e-5, "dx")
+    assert_close_scaled(layer.W.grad.cpu().numpy(), dW, 1e-5, "dW")
+    assert_close_scaled(layer.gamma.grad.cpu().numpy(), dg, 1e-5, "dgamma")
+    assert_close_scaled(layer.beta.grad.cpu().numpy(), db, 1e-5, "dbeta")
