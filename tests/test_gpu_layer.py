@@ -161,12 +161,14 @@ def test_routing_rule():
     and the 8-GPU shard on the streamed ones; PSN_STREAM overrides."""
     from paper_2501_14490_b200 import _lib as L
     base = L.PSN_QUANTIZED | L.PSN_USE_BATCH_STATS
-    for shape, k, d, want in [((250, 32, 128), 4, 1, 0), ((1024, 64, 512), 8, 3, 0), ((1024, 64, 512), 4, 1, 1),
-                              ((1024, 8, 512), 4, 3, 1), ((1024, 64, 512), 6, 3, 1)]:
+    for shape, k, d, dt, want in [((250, 32, 128), 4, 1, torch.float32, 0), ((1024, 64, 512), 8, 3, torch.float32, 0),
+                                  ((1024, 64, 512), 4, 1, torch.float32, 1), ((1024, 8, 512), 4, 3, torch.float32, 1),
+                                  ((1024, 64, 512), 6, 3, torch.float32, 1), ((1024, 64, 512), 8, 3, torch.bfloat16, 1),
+                                  ((250, 32, 128), 4, 1, torch.bfloat16, 0)]:
         for bwd in (False, True):
-            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base), bwd)["streamed"] == want, shape
-            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base | L.PSN_STREAM), bwd)["streamed"] == 1
-            assert L.plan_info(L.make_desc(shape, k, d, torch.float32, flags=base | L.PSN_GENERIC), bwd)["streamed"] == 0
+            assert L.plan_info(L.make_desc(shape, k, d, dt, flags=base), bwd)["streamed"] == want, (shape, dt)
+            assert L.plan_info(L.make_desc(shape, k, d, dt, flags=base | L.PSN_STREAM), bwd)["streamed"] == 1
+            assert L.plan_info(L.make_desc(shape, k, d, dt, flags=base | L.PSN_GENERIC), bwd)["streamed"] == 0
 
 
 @pytest.mark.parametrize("d", [1, 2, 3])
