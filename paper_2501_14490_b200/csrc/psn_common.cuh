@@ -168,11 +168,13 @@ __device__ __forceinline__ void stream_col(const IO* px, const IO* pq, int64_t s
 // registers.
 constexpr int kRingSteps = 32;
 
+// per-lane copies need a 4 / 8 B element (cp.async has no 2-byte form); bf16
+// rings run in the 16-byte-piece mode only
 template <typename IO>
-__host__ __device__ constexpr bool ring_streamed() { return sizeof(IO) >= 4; }  // cp.async moves 4 / 8 / 16 B
+__host__ __device__ constexpr bool ring_scalar_ok() { return sizeof(IO) >= 4; }
 template <typename IO>
 __host__ __device__ constexpr size_t ring_bytes(int streams) {  // dynamic shared memory of one block
-  return ring_streamed<IO>() ? (size_t)streams * kWarps * kRingSteps * 32 * sizeof(IO) : 0;
+  return (size_t)streams * kWarps * kRingSteps * 32 * sizeof(IO);
 }
 
 template <int BYTES>
@@ -243,7 +245,7 @@ __device__ __forceinline__ void stream_ring(IO* rx, IO* rq, const ColTile& ct, c
           cp_async_elem<16>(rx + (base + u) * 32 + pc * EPP, ok ? vx + e : gx, ok);
           if (DY) cp_async_elem<16>(rq + (base + u) * 32 + pc * EPP, ok ? vq + e : gq, ok);
         }
-      } else {
+      } else if constexpr (ring_scalar_ok<IO>()) {
 #pragma unroll
         for (int u = 0; u < kRingCH; ++u) {
           const bool ok = ct.jv && tb + u < lim;
@@ -284,17 +286,25 @@ __device__ __forceinline__ void stream_ring(IO* rx, IO* rq, const ColTile& ct, c
 }
 
 // the streaming loop of the generic kernels: the shared-memory ring for 4 / 8 B
-// carriers, the register prefetch for bf16.  `ring` is this warp's slice of
-// the block's dynamic shared memory (2 streams when DY).  CH: steps per
-// chunk (unrolled; 4 for the register-heavy high orders).
+// carriers, and for bf16 tiles that move as 16-byte pieces (8 rows per warp
+// copy, so chunks of 8); the register prefetch for the other bf16 tiles.
+// `ring` is this warp's slice of the block's dynamic shared memory (2
+// streams when DY).  CH: steps per chunk (unrolled; 4 for the register-heavy
+// high orders).
 template <int CH, bool DY, typename IO, typename F>
 __device__ __forceinline__ void stream_any(IO* ring, const ColTile& ct, const IO* px, const IO* pq, const IO* gx,
                                            const IO* gq, int64_t step, int64_t t0, int64_t t1, int64_t lim,
                                            F&& f) {
-  if constexpr (ring_streamed<IO>())
+  if constexpr (ring_scalar_ok<IO>()) {
     stream_ring<CH, DY>(ring, ring + kRingSteps * 32, ct, px, pq, gx, gq, step, t0, t1, lim, f);
-  else
+  } else if constexpr (CH % 8 == 0) {
+    if (ct.vec)
+      stream_ring<CH, DY>(ring, ring + kRingSteps * 32, ct, px, pq, gx, gq, step, t0, t1, lim, f);
+    else
+      stream_col<4, DY>(px, pq, step, t0, t1, lim, ct.jv, f);
+  } else {
     stream_col<4, DY>(px, pq, step, t0, t1, lim, ct.jv, f);
+  }
 }
 
 __device__ __forceinline__ float load_f(const float* p) { return __ldg(p); }
@@ -377,10 +387,11 @@ int check_ptr(const void* p, size_t align, const char* what);
 size_t dtype_size(int dt);
 size_t workspace_part3_offset(const psn_desc_t* desc);
 
-// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
+// static + dynamic shared memory above the 48 KB default needs the per-kernel
+// opt-in (the rings add to kernels that also hold static reduction buffers)
 template <typename Kern>
 int smem_optin(Kern* kern, size_t bytes) {
-  if (bytes <= 48 * 1024) return PSN_OK;
+  if (bytes == 0) return PSN_OK;
   if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
       cudaSuccess)
     return fail(PSN_ERR_CUDA, "cudaFuncSetAttribute (generic kernel smem) failed");

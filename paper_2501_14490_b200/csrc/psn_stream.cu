@@ -77,14 +77,13 @@ bool eligible(const psn_desc_t* desc) {
 // on B200 (profiles/r2_route.txt, CUDA-graph replay of fwd+bwd): below ~1.5M
 // elements the streamed kernel's cross-CTA synchronisation skeleton costs more
 // than the whole generic pass (BASELINE config 1, 1.0M elements: 0.049 vs
-// 0.039 ms), and with f32 I/O the widest windows ((k-1) d > 16: k = 8, d = 3)
-// spill registers in the streamed kernels (0.72 vs 0.51 ms; with bf16 I/O the
-// generic kernels have no cp.async ring and lose: 0.60 streamed vs 0.73 ms).
-// PSN_STREAM in the descriptor skips this preference.
+// 0.039 ms), and the widest windows ((k-1) d > 16: k = 8, d = 3) spill
+// registers in the streamed kernels (f32 0.72 vs 0.51 ms, bf16 0.60 vs 0.53 ms
+// at T=1024, B=64, C=512).  PSN_STREAM in the descriptor skips this preference.
 bool prefer_generic(const psn_desc_t* desc) {
   if (desc->flags & PSN_STREAM) return false;
   if ((double)desc->T * desc->N * desc->C * desc->Q < 1.5e6) return true;
-  return desc->dtype == PSN_F32 && (desc->k - 1) * desc->d > 16;
+  return (desc->k - 1) * desc->d > 16;
 }
 
 bool shape_eligible(const psn_desc_t* desc) {
