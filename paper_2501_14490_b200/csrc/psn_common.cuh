@@ -289,8 +289,9 @@ __device__ __forceinline__ void stream_ring(IO* rx, IO* rq, const ColTile& ct, c
 // carriers, and for bf16 tiles that move as 16-byte pieces (8 rows per warp
 // copy, so chunks of 8); the register prefetch for the other bf16 tiles.
 // `ring` is this warp's slice of the block's dynamic shared memory (2
-// streams when DY).  CH: steps per chunk (unrolled; 4 for the register-heavy
-// high orders).
+// streams when DY).  CH: steps per chunk (unrolled; 8 at every order: at
+// k = 16 the longer unroll beats the lower register pressure of 4,
+// k = 16 d = 3 f32 0.81 -> 0.77 ms).
 template <int CH, bool DY, typename IO, typename F>
 __device__ __forceinline__ void stream_any(IO* ring, const ColTile& ct, const IO* px, const IO* pq, const IO* gx,
                                            const IO* gq, int64_t step, int64_t t0, int64_t t1, int64_t lim,

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_stats_kernel(Ge
     prime_window<K>(xw, base, step, s.s0, jv);
     const IO* p = base + s.s0 * step;
     double k0 = 0.0, s1 = 0.0, s2 = 0.0;  // k0: the segment's first h1, shift for the moments
-    stream_any<(K > 8 && sizeof(IO) >= 4 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t t, int64_t) {
+    stream_any<8, false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t t, int64_t) {
       push<K>(xw, wide(xv));
       const double h1 = Carrier<IO>::round(conv_taps2<K>(w, xw));
       if (t == s.s0) k0 = h1;
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, (K > 8 ? 1 : 2)) fwd_spike_kernel(Ge
     }
     const IO* p = base + s.s0 * step;
     IO* o = out + off + s.s0 * step;
-    stream_any<(K > 8 && sizeof(IO) >= 4 ? 4 : 8), false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t, int64_t eo) {
+    stream_any<8, false>(ring, ct, p, p, x, x, step, s.s0, s.s1, s.s1, [&](IO xv, IO, int64_t, int64_t eo) {
       double v = wide(xv);
       if (MODE == 2) v = Carrier<IO>::to_f32(v);
       push<K>(xw, v);
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(Geom g, const IO* 
     const IO* p = x + off + s.s0 * step;
     const IO* q = dy + off + s.s0 * step;
     float* dm = dhm ? dhm + off + s.s0 * step : nullptr;  // materialised dh2 | h1 - mu for bwd_dx_mat
-    stream_any<(K > 8 && sizeof(IO) >= 4 ? 4 : 8), true>(ring, ct, p, q, x, dy, step, s.s0, s.s1, s.s1, [&](IO xv, IO dv, int64_t, int64_t eo) {
+    stream_any<8, true>(ring, ct, p, q, x, dy, step, s.s0, s.s1, s.s1, [&](IO xv, IO dv, int64_t, int64_t eo) {
       const double v = wide(xv);
       push<K>(xw, v);
       xsum += v;
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(kThreads) bwd_dx_kernel(Geom g, const IO* __re
     IO* o = dx + off + (s.s0 - (K - 1)) * step;
     const int64_t tend = s.s1 + K - 1;
     const int64_t lim = tend < s.Sr ? tend : s.Sr;
-    stream_any<(K > 8 && sizeof(IO) >= 4 ? 4 : 8), true>(ring, ct, p, q, x, dy, step, s.s0, tend, lim, [&](IO xv, IO dv, int64_t t, int64_t eo) {
+    stream_any<8, true>(ring, ct, p, q, x, dy, step, s.s0, tend, lim, [&](IO xv, IO dv, int64_t t, int64_t eo) {
       Acc dh2 = (Acc)0, dh1 = (Acc)0;
       if (t < s.Sr) {
         push<K>(xw, wide(xv));
