@@ -671,7 +671,10 @@ def main():
                               "bytes_per_step": 5 * esize * nel, "fwd_ms": f_ms, "bwd_ms": b_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * (wl.plan_f["launches"] + wl.plan_b["launches"]),
+            # kernels of this repo per timed step (the streamed plans' workspace
+            # memset is a driver memset node, not counted)
+            "gpu_launches": K * sum(pl["launches"] - (1 if pl.get("streamed") else 0)
+                                    for pl in (wl.plan_f, wl.plan_b)),
             "plan": {"forward": wl.plan_f, "backward": wl.plan_b},
             "clocks": clk.summary(),
             "wall_s_timed": wall,
