@@ -182,11 +182,14 @@ class SpikingNet(nn.Module):
         return out
 
     def zero_grad(self, set_to_none: bool = False) -> None:
+        live = []
         for p in self.parameters_list():
             if set_to_none or p.grad is None:
                 p.grad = None if set_to_none else torch.zeros_like(p)
             else:
-                p.grad.zero_()
+                live.append(p.grad)
+        if live:
+            torch._foreach_zero_(live)  # one multi-tensor launch instead of one fill per parameter
 
     def forward(self, x: torch.Tensor, mode: Mode = Mode.TRAIN) -> torch.Tensor:
         h = x
